@@ -1,0 +1,265 @@
+/*
+ * dfuse_cuda.h -- C-ABI of the B200 implementation of DeepFusion's per-frame
+ * dense-depth hot path (texture mask -> epipolar SSD search -> semi-dense
+ * update -> alternating Gauss-Newton fusion with Huber IRLS + Jacobi PCG).
+ *
+ * Every entry point replaces one function of the reference's header-only
+ * C++ API (/root/reference/proj/include/dfuse, cited per entry point below as
+ * file:line). Conventions:
+ *   - plain pointers and sizes only; no C++ or torch types;
+ *   - every raster is row-major, index i = y*W + x (raster.hpp:11-12,30);
+ *   - pointers are HOST pointers unless the name ends in _dev;
+ *   - return value 0 = OK, otherwise (int)dfuse::Err + 1 (errors.hpp:8-42);
+ *     dfuse_last_error() returns the message of the last failing call;
+ *   - one dfuse_ctx = one device + one stream; not thread-safe; distinct
+ *     contexts may run concurrently; every call is synchronous;
+ *   - there is no CPU fallback: a context cannot be created without an sm_100
+ *     device and every compute call runs a CUDA kernel.
+ */
+#ifndef DFUSE_CUDA_H
+#define DFUSE_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DFUSE_ABI_VERSION 1
+
+/* error codes = (int)dfuse::Err + 1, errors.hpp:8-42 */
+enum {
+  DFUSE_OK = 0,
+  DFUSE_E_NON_POSITIVE_DEPTH = 1,
+  DFUSE_E_BEHIND_CAMERA = 2,
+  DFUSE_E_OUT_OF_BOUNDS = 3,
+  DFUSE_E_DEGENERATE_BASELINE = 4,
+  DFUSE_E_NO_MINIMUM = 5,
+  DFUSE_E_ZERO_BASELINE_STEP = 6,
+  DFUSE_E_DEGENERATE_JACOBIAN = 7,
+  DFUSE_E_BORDER_PIXEL = 8,
+  DFUSE_E_BAD_MAGIC = 9,
+  DFUSE_E_DIMENSION_MISMATCH = 10,
+  DFUSE_E_NON_POSITIVE_VARIANCE = 11,
+  DFUSE_E_TRUNCATED_FILE = 12,
+  DFUSE_E_NON_POSITIVE_FOCAL = 13,
+  DFUSE_E_NON_POSITIVE_GROUND_TRUTH = 14,
+  DFUSE_E_MISSING_FILE = 15,
+  DFUSE_E_MALFORMED_LINE = 16,
+  DFUSE_E_NON_UNIT_QUATERNION = 17,
+  DFUSE_E_BAD_IMAGE_FORMAT = 18,
+  DFUSE_E_NON_POSITIVE_SCALE = 19,
+  DFUSE_E_CG_DIVERGENCE = 20,
+  DFUSE_E_NO_SEMIDENSE_SUPPORT = 21,
+  DFUSE_E_NO_VALID_GROUND_TRUTH = 22,
+  DFUSE_E_MISMATCHED_KEYFRAME_SETS = 23,
+  DFUSE_E_IO_ERROR = 24,
+  DFUSE_E_UNKNOWN_KEY = 25,
+  DFUSE_E_TYPE_ERROR = 26,
+  DFUSE_E_INVALID_ARGUMENT = 27,
+  DFUSE_E_CUDA = 100 /* CUDA runtime failure (not a reference error) */
+};
+
+/* EpipolarStatus, semidense.hpp:46-53 */
+enum {
+  DFUSE_EPI_OK = 0,
+  DFUSE_EPI_DEGENERATE_BASELINE = 1,
+  DFUSE_EPI_OUT_OF_BOUNDS = 2,
+  DFUSE_EPI_BEHIND_CAMERA = 3,
+  DFUSE_EPI_NO_MINIMUM = 4,
+  DFUSE_EPI_DEGENERATE_JACOBIAN = 5,
+  DFUSE_EPI_NOT_SEARCHED = -1 /* pixel outside the texture mask (debug output only) */
+};
+
+/* FusionMode, fusion.hpp:33 */
+enum { DFUSE_MODE_FULL = 0, DFUSE_MODE_NOPAIRWISE = 1, DFUSE_MODE_LSSCALE = 2 };
+
+/* CameraIntrinsics, geometry.hpp:18-41 */
+typedef struct {
+  double fx, fy, cx, cy;
+  int32_t width, height;
+} dfuse_intrinsics;
+
+/* EpipolarGeometry, semidense.hpp:94-99. R_10 row-major. */
+typedef struct {
+  double R_10[9];
+  double t_10[3];
+  double t_01[3];
+  dfuse_intrinsics K;
+} dfuse_epigeom;
+
+/* SearchConfig, semidense.hpp:66-73 (defaults 0.25, 50, 0.05) */
+typedef struct {
+  double min_depth, max_depth, max_rms_error;
+} dfuse_search_cfg;
+
+/* RobustConfig, fusion.hpp:23-31 (defaults 0.3, 0.3, 0.1, 10, 1e-6, 200, 1) */
+typedef struct {
+  double delta_semi, delta_net, delta_grad;
+  double cg_tol;
+  int32_t gn_iterations;
+  int32_t cg_max_iters;
+  int32_t estimate_scale;
+  int32_t reserved;
+} dfuse_robust_cfg;
+
+/* EpipolarObservation, semidense.hpp:38-44 (112 bytes, same field order) */
+typedef struct {
+  double x, y;
+  double depth;
+  double error5[5];
+  double jacobian[5];
+  double variance;
+} dfuse_obs;
+
+/* Dense fusion problem (FusionState inputs other than log_depth/scale,
+ * SemiDenseMap semidense.hpp:21-31, PredictionSet predictions.hpp:18-29).
+ * pred[c], c = log_depth, log_depth_var, grad_x, grad_x_var, grad_y,
+ * grad_y_var. Host pointers, W*H entries each. */
+typedef struct {
+  int32_t width, height;
+  const double* semi_depth;
+  const double* semi_variance;
+  const uint8_t* semi_valid;
+  int32_t inlier_count;
+  int32_t reserved;
+  const double* pred[6];
+} dfuse_fusion_inputs;
+
+/* Solver trace of one optimize() call (fusion.hpp:402-454). Per-GN arrays
+ * are recorded for the first DFUSE_STATS_MAX_GN iterations. */
+#define DFUSE_STATS_MAX_GN 512
+typedef struct {
+  int32_t gn_done;      /* GN iterations executed */
+  int32_t pcg_total;    /* PCG iterations summed over GN iterations */
+  int32_t cost_evals;   /* total_cost sweeps (incl. line-search trials) */
+  int32_t grid_syncs;   /* device-wide barriers executed */
+  int32_t pcg_iters[DFUSE_STATS_MAX_GN];   /* -1: depth block not run */
+  double scale_step[DFUSE_STATS_MAX_GN];   /* accepted step; 0 none; -1 not run */
+  double depth_step[DFUSE_STATS_MAX_GN];   /* accepted step; 0 none; -1 not run */
+} dfuse_solver_stats;
+
+typedef struct dfuse_ctx dfuse_ctx;
+typedef struct dfuse_keyframe dfuse_keyframe;
+
+/* ---- context ---------------------------------------------------------- */
+int dfuse_abi_version(void);
+const char* dfuse_err_name(int code); /* err_name, errors.hpp:44-75 */
+int dfuse_ctx_create(int device, dfuse_ctx** out);
+int dfuse_ctx_destroy(dfuse_ctx* ctx);
+const char* dfuse_last_error(const dfuse_ctx* ctx);
+/* number of persistent CTAs the fusion solver uses (0 = one per SM) */
+int dfuse_ctx_set_solver_ctas(dfuse_ctx* ctx, int ctas);
+/* kernels launched on this context since creation (evidence counter) */
+int64_t dfuse_ctx_launch_count(const dfuse_ctx* ctx);
+/* the context's cudaStream_t (for timing with events on the launch stream) */
+void* dfuse_ctx_stream(const dfuse_ctx* ctx);
+
+/* ---- host-side geometry ------------------------------------------------
+ * make_epipolar_geometry(T0, T1, K), semidense.hpp:101-106, with Pose =
+ * (quaternion w,x,y,z ; translation), geometry.hpp:44-67. Pure host code:
+ * per frame pair, 15 doubles. */
+int dfuse_make_epipolar_geometry(const double q0_wxyz[4], const double t0[3],
+                                 const double q1_wxyz[4], const double t1[3],
+                                 const dfuse_intrinsics* K, dfuse_epigeom* out);
+
+/* ---- stereo front end (semidense.hpp) -------------------------------- */
+/* texture_mask(img, threshold), semidense.hpp:77-91 */
+int dfuse_texture_mask(dfuse_ctx* ctx, const float* img, int width, int height, double threshold,
+                       uint8_t* mask);
+
+/* search_depth(g, I0, I1, x, prior, cfg), semidense.hpp:277-379, for a list
+ * of n pixels. px: n (x,y) pairs. prior: n (depth, sigma) pairs or NULL;
+ * has_prior: n flags or NULL (NULL with prior != NULL means all have one).
+ * Outputs: status[n] (DFUSE_EPI_*), obs[n] (valid where status == OK),
+ * optional best[n] / n_steps[n] (search index of the SSD minimum and the
+ * number of steps; -1 where the search did not reach that point). */
+int dfuse_search_depth(dfuse_ctx* ctx, const dfuse_epigeom* g, const float* I0, const float* I1,
+                       int n, const double* px, const double* prior, const uint8_t* has_prior,
+                       const dfuse_search_cfg* cfg, int32_t* status, dfuse_obs* obs,
+                       int32_t* best, int32_t* n_steps);
+
+/* update_semidense(map, observations), semidense.hpp:393-417. The map is
+ * updated in place (depth, variance, valid, inlier_count). Observations are
+ * applied in list order (duplicates of one pixel fuse sequentially). */
+int dfuse_update_semidense(dfuse_ctx* ctx, int width, int height, double* depth, double* variance,
+                           uint8_t* valid, int32_t* inlier_count, int n_obs, const dfuse_obs* obs);
+
+/* stereo_scan + update_semidense fused (pipeline.hpp:157-190,207-212): every
+ * masked pixel searched with the prior taken from the map, then fused into
+ * the map in place. n_obs = number of OK observations. Optional outputs
+ * (NULL to skip): per-pixel status (int8, DFUSE_EPI_NOT_SEARCHED off-mask),
+ * best, n_steps, and the observation list in raster order (capacity W*H). */
+int dfuse_stereo_update(dfuse_ctx* ctx, const dfuse_epigeom* g, const float* I0, const float* I1,
+                        const uint8_t* mask, const dfuse_search_cfg* cfg, double* depth,
+                        double* variance, uint8_t* valid, int32_t* inlier_count, int32_t* n_obs,
+                        int8_t* status, int32_t* best, int32_t* n_steps, dfuse_obs* obs);
+
+/* ---- fusion optimiser (fusion.hpp) ----------------------------------- */
+/* assemble_normal_equations, fusion.hpp:171-222 */
+int dfuse_assemble_normal_equations(dfuse_ctx* ctx, const dfuse_fusion_inputs* in,
+                                    const double* log_depth, double scale,
+                                    const dfuse_robust_cfg* cfg, int mode, double* diag,
+                                    double* right, double* down, double* b);
+/* total_cost, fusion.hpp:225-253 */
+int dfuse_total_cost(dfuse_ctx* ctx, const dfuse_fusion_inputs* in, const double* log_depth,
+                     double scale, const dfuse_robust_cfg* cfg, int mode, double* cost);
+/* cost_gradient, fusion.hpp:263-308 */
+int dfuse_cost_gradient(dfuse_ctx* ctx, const dfuse_fusion_inputs* in, const double* log_depth,
+                        double scale, const dfuse_robust_cfg* cfg, int mode, double* cost,
+                        double* wrt_log_depth, double* wrt_ln_scale);
+/* StencilMatrix::apply, fusion.hpp:120-135 */
+int dfuse_stencil_apply(dfuse_ctx* ctx, int width, int height, const double* diag,
+                        const double* right, const double* down, const double* x, double* y);
+/* solve_depth_step, fusion.hpp:316-368. iterations: PCG iterations run. */
+int dfuse_solve_depth_step(dfuse_ctx* ctx, int width, int height, const double* diag,
+                           const double* right, const double* down, const double* b,
+                           const dfuse_robust_cfg* cfg, double* delta, int32_t* iterations);
+/* solve_scale_step, fusion.hpp:373-391 */
+int dfuse_solve_scale_step(dfuse_ctx* ctx, const dfuse_fusion_inputs* in, const double* log_depth,
+                           double scale, const dfuse_robust_cfg* cfg, double* scale_out);
+/* optimize, fusion.hpp:402-454. Transactional: log_depth/scale/iteration are
+ * written only when the call returns DFUSE_OK. stats may be NULL. */
+int dfuse_optimize(dfuse_ctx* ctx, const dfuse_fusion_inputs* in, double* log_depth,
+                   double* scale, int32_t* iteration, const dfuse_robust_cfg* cfg, int mode,
+                   dfuse_solver_stats* stats);
+
+/* ---- device-resident keyframe session (pipeline.hpp:125-228) ---------- */
+/* Result of one tracked frame through process_frame (pipeline.hpp:194-228)
+ * with keyframe retirement disabled. */
+typedef struct {
+  int32_t observations;   /* ProcessOutcome::observations */
+  int32_t inlier_count;   /* SemiDenseMap::inlier_count after the update */
+  int32_t stereo_frames;  /* Keyframe::stereo_frames */
+  int32_t optimize_status;/* DFUSE_OK, or the error optimize threw (state unchanged) */
+  float stereo_ms;        /* device time of the stereo stage */
+  float optimise_ms;      /* device time of the optimise stage */
+  dfuse_solver_stats stats;
+} dfuse_frame_result;
+
+/* make_keyframe (pipeline.hpp:125-153) minus prediction I/O: uploads I0 and
+ * the six prediction planes, computes the texture mask, empties the
+ * semi-dense map and sets the fusion state to init_state(pred). */
+int dfuse_kf_create(dfuse_ctx* ctx, const dfuse_intrinsics* K, const float* I0,
+                    const double* const pred[6], double texture_threshold, dfuse_keyframe** out);
+int dfuse_kf_destroy(dfuse_keyframe* kf);
+/* restore the just-created state (device-to-device copies) */
+int dfuse_kf_reset(dfuse_keyframe* kf);
+/* process_frame for a tracked frame: stereo scan + update + optimize.
+ * I1 is a host image (copied in); _dev takes a device pointer. */
+int dfuse_kf_process_frame(dfuse_keyframe* kf, const dfuse_epigeom* g, const float* I1,
+                           const dfuse_search_cfg* scfg, const dfuse_robust_cfg* rcfg, int mode,
+                           dfuse_frame_result* res);
+int dfuse_kf_process_frame_dev(dfuse_keyframe* kf, const dfuse_epigeom* g, const float* I1_dev,
+                               const dfuse_search_cfg* scfg, const dfuse_robust_cfg* rcfg,
+                               int mode, dfuse_frame_result* res);
+/* copy state back to the host (any pointer may be NULL) */
+int dfuse_kf_download(dfuse_keyframe* kf, double* log_depth, double* scale, int32_t* iteration,
+                      double* semi_depth, double* semi_variance, uint8_t* semi_valid,
+                      int32_t* inlier_count, uint8_t* mask);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DFUSE_CUDA_H */

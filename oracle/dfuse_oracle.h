@@ -1,0 +1,83 @@
+/*
+ * dfuse_oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * CPU restatement of the reference's hot path, used as the parity checker
+ * for the CUDA implementation. Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline leg may load it; the product path
+ * (paper_2207_12244_b200/) never links or calls it.
+ *
+ * Two libraries export this exact function set:
+ *   orc_*  oracle/dfuse_oracle.c  -- plain-C restatement, single thread
+ *   ref_*  oracle/ref_driver.cpp  -- the reference's own headers from
+ *          /root/reference/proj/include compiled unmodified (+ OpenMP)
+ *          against include/compat/Eigen; built into oracle/_ref/.
+ * tests/test_oracle_pin.py checks orc_* == ref_* bit for bit on seeded
+ * inputs, which pins the restatement to the reference.
+ *
+ * Types and error codes are those of include/dfuse_cuda.h.
+ */
+#ifndef DFUSE_ORACLE_H
+#define DFUSE_ORACLE_H
+
+#include "../include/dfuse_cuda.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DFUSE_ORACLE_DECLS(P)                                                                     \
+  int P##make_epipolar_geometry(const double q0_wxyz[4], const double t0[3],                     \
+                                const double q1_wxyz[4], const double t1[3],                     \
+                                const dfuse_intrinsics* K, dfuse_epigeom* out);                  \
+  int P##texture_mask(const float* img, int width, int height, double threshold, uint8_t* mask); \
+  int P##search_depth(const dfuse_epigeom* g, const float* I0, const float* I1, int n,           \
+                      const double* px, const double* prior, const uint8_t* has_prior,          \
+                      const dfuse_search_cfg* cfg, int32_t* status, dfuse_obs* obs,             \
+                      int32_t* best, int32_t* n_steps);                                          \
+  int P##update_semidense(int width, int height, double* depth, double* variance,               \
+                          uint8_t* valid, int32_t* inlier_count, int n_obs,                     \
+                          const dfuse_obs* obs);                                                 \
+  int P##stereo_update(const dfuse_epigeom* g, const float* I0, const float* I1,                 \
+                       const uint8_t* mask, const dfuse_search_cfg* cfg, double* depth,         \
+                       double* variance, uint8_t* valid, int32_t* inlier_count, int32_t* n_obs, \
+                       int8_t* status, int32_t* best, int32_t* n_steps, dfuse_obs* obs);        \
+  int P##assemble_normal_equations(const dfuse_fusion_inputs* in, const double* log_depth,      \
+                                   double scale, const dfuse_robust_cfg* cfg, int mode,         \
+                                   double* diag, double* right, double* down, double* b);       \
+  int P##total_cost(const dfuse_fusion_inputs* in, const double* log_depth, double scale,       \
+                    const dfuse_robust_cfg* cfg, int mode, double* cost);                       \
+  int P##cost_gradient(const dfuse_fusion_inputs* in, const double* log_depth, double scale,    \
+                       const dfuse_robust_cfg* cfg, int mode, double* cost,                     \
+                       double* wrt_log_depth, double* wrt_ln_scale);                            \
+  int P##stencil_apply(int width, int height, const double* diag, const double* right,          \
+                       const double* down, const double* x, double* y);                         \
+  int P##solve_depth_step(int width, int height, const double* diag, const double* right,       \
+                          const double* down, const double* b, const dfuse_robust_cfg* cfg,     \
+                          double* delta, int32_t* iterations);                                  \
+  int P##solve_scale_step(const dfuse_fusion_inputs* in, const double* log_depth, double scale, \
+                          const dfuse_robust_cfg* cfg, double* scale_out);                      \
+  int P##optimize(const dfuse_fusion_inputs* in, double* log_depth, double* scale,              \
+                  int32_t* iteration, const dfuse_robust_cfg* cfg, int mode,                    \
+                  dfuse_solver_stats* stats);
+
+DFUSE_ORACLE_DECLS(orc_)
+DFUSE_ORACLE_DECLS(ref_)
+
+/* ref_ only: one tracked frame through the reference's process_frame
+ * (pipeline.hpp:194-228) with retirement disabled, timed per stage like
+ * StageTimer (pipeline.hpp:101-115). Returns the optimize error code (the
+ * fusion state is unchanged on error, as in run_sequence). */
+int ref_process_frame(const dfuse_epigeom* g, const float* I0, const float* I1,
+                      const uint8_t* mask, const dfuse_search_cfg* scfg,
+                      const dfuse_fusion_inputs* in_pred_only, double* semi_depth,
+                      double* semi_variance, uint8_t* semi_valid, int32_t* inlier_count,
+                      double* log_depth, double* scale, int32_t* iteration,
+                      const dfuse_robust_cfg* rcfg, int mode, int32_t* n_obs,
+                      double* stereo_ms, double* optimise_ms);
+int ref_omp_max_threads(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,183 @@
+"""Python mirror of the reference API, bound to the CUDA library.
+
+``cuda()`` returns a :class:`Bindings` over ``libdfuse_cuda.so`` (the
+``dfuse_*`` C-ABI of include/dfuse_cuda.h) with methods named like the
+reference's functions: texture_mask, search_depth, update_semidense,
+stereo_update (stereo_scan + update_semidense), assemble_normal_equations,
+total_cost, cost_gradient, stencil_apply, solve_depth_step,
+solve_scale_step, optimize. :class:`Keyframe` is the device-resident
+session (make_keyframe + process_frame, pipeline.hpp:125-228).
+
+There is no CPU fallback: if the library is missing or no sm_100 device is
+visible, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from ._ffi import (Bindings, DfuseError, EpiGeom, FrameResultC, Intrinsics, PredictionSet,
+                   RobustConfig, SearchConfig, SemiDenseMap, SolverStats, FusionState, _f32,
+                   _f64, _mode)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdfuse_cuda.so")
+
+_lib = None
+_default = {}
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; "
+                               f"g.build()'` (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        L.dfuse_ctx_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+        L.dfuse_ctx_create.restype = C.c_int
+        L.dfuse_ctx_destroy.argtypes = [C.c_void_p]
+        L.dfuse_last_error.argtypes = [C.c_void_p]
+        L.dfuse_last_error.restype = C.c_char_p
+        L.dfuse_ctx_set_solver_ctas.argtypes = [C.c_void_p, C.c_int]
+        L.dfuse_ctx_launch_count.argtypes = [C.c_void_p]
+        L.dfuse_ctx_launch_count.restype = C.c_int64
+        L.dfuse_err_name.restype = C.c_char_p
+        L.dfuse_ctx_stream.argtypes = [C.c_void_p]
+        L.dfuse_ctx_stream.restype = C.c_void_p
+        L.dfuse_kf_create.argtypes = [C.c_void_p, C.POINTER(Intrinsics), C.c_void_p,
+                                      C.POINTER(C.c_void_p), C.c_double, C.POINTER(C.c_void_p)]
+        L.dfuse_kf_destroy.argtypes = [C.c_void_p]
+        L.dfuse_kf_reset.argtypes = [C.c_void_p]
+        for name in ("dfuse_kf_process_frame", "dfuse_kf_process_frame_dev"):
+            f = getattr(L, name)
+            f.argtypes = [C.c_void_p, C.POINTER(EpiGeom), C.c_void_p, C.c_void_p, C.c_void_p,
+                          C.c_int, C.POINTER(FrameResultC)]
+        L.dfuse_kf_download.argtypes = [C.c_void_p] + [C.c_void_p] * 8
+        _lib = L
+    return _lib
+
+
+class Context:
+    """One device + one stream (dfuse_ctx)."""
+
+    def __init__(self, device: int = 0):
+        L = lib()
+        h = C.c_void_p()
+        rc = L.dfuse_ctx_create(int(device), C.byref(h))
+        if rc != 0:
+            raise DfuseError(rc, f"dfuse_ctx_create(device={device}): no usable sm_100 device")
+        self.handle = h
+        self.device = device
+        self.api = Bindings(L, "dfuse_", h, "cuda")
+
+    def set_solver_ctas(self, n: int) -> None:
+        lib().dfuse_ctx_set_solver_ctas(self.handle, int(n))
+
+    def stream_handle(self) -> int:
+        """cudaStream_t the library launches on (wrap with torch.cuda.ExternalStream)."""
+        return int(lib().dfuse_ctx_stream(self.handle))
+
+    def launch_count(self) -> int:
+        return int(lib().dfuse_ctx_launch_count(self.handle))
+
+    def close(self) -> None:
+        if self.handle:
+            lib().dfuse_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def context(device: int = 0) -> Context:
+    if device not in _default:
+        _default[device] = Context(device)
+    return _default[device]
+
+
+def cuda(device: int = 0) -> Bindings:
+    """The reference-shaped API on the GPU (default context of `device`)."""
+    return context(device).api
+
+
+class Keyframe:
+    """Device-resident keyframe (dfuse_keyframe): make_keyframe on creation,
+    process_frame per tracked frame, download() for the state."""
+
+    def __init__(self, ctx: Context, camera, I0, pred: PredictionSet,
+                 texture_threshold: float = 0.02):
+        L = lib()
+        self.ctx = ctx
+        self.W, self.H = camera.width, camera.height
+        self._I0 = _f32(I0)
+        self._planes = pred.planes()
+        arr = (C.c_void_p * 6)(*[p.ctypes.data for p in self._planes])
+        kc = camera.c()
+        h = C.c_void_p()
+        rc = L.dfuse_kf_create(ctx.handle, C.byref(kc), self._I0.ctypes.data, arr,
+                               float(texture_threshold), C.byref(h))
+        if rc != 0:
+            raise DfuseError(rc, L.dfuse_last_error(ctx.handle).decode())
+        self.handle = h
+
+    def _check(self, rc, what):
+        if rc != 0:
+            raise DfuseError(rc, f"{what}: " + lib().dfuse_last_error(self.ctx.handle).decode())
+
+    def reset(self):
+        self._check(lib().dfuse_kf_reset(self.handle), "dfuse_kf_reset")
+
+    def process_frame(self, g: EpiGeom, I1, search: SearchConfig | None = None,
+                      robust: RobustConfig | None = None, mode="full", device_ptr=None):
+        """One tracked frame: stereo scan + semi-dense update + optimize.
+        `I1` is a host image, or pass `device_ptr` (int) of a float32 device
+        image. Returns the dfuse_frame_result struct."""
+        search = search or SearchConfig()
+        robust = robust or RobustConfig()
+        sc, rc_ = search.c(), robust.c()
+        res = FrameResultC()
+        L = lib()
+        if device_ptr is not None:
+            rc = L.dfuse_kf_process_frame_dev(self.handle, C.byref(g), C.c_void_p(device_ptr),
+                                              C.byref(sc), C.byref(rc_), _mode(mode),
+                                              C.byref(res))
+        else:
+            img = _f32(I1)
+            rc = L.dfuse_kf_process_frame(self.handle, C.byref(g), img.ctypes.data, C.byref(sc),
+                                          C.byref(rc_), _mode(mode), C.byref(res))
+        self._check(rc, "dfuse_kf_process_frame")
+        return res
+
+    def download(self):
+        """-> (FusionState, SemiDenseMap, mask)"""
+        h, w = self.H, self.W
+        ld = np.zeros((h, w))
+        sd, sv = np.zeros((h, w)), np.zeros((h, w))
+        valid = np.zeros((h, w), np.uint8)
+        mask = np.zeros((h, w), np.uint8)
+        scale = C.c_double(0)
+        it = C.c_int32(0)
+        cnt = C.c_int32(0)
+        self._check(lib().dfuse_kf_download(self.handle, ld.ctypes.data, C.addressof(scale),
+                                            C.addressof(it), sd.ctypes.data, sv.ctypes.data,
+                                            valid.ctypes.data, C.addressof(cnt),
+                                            mask.ctypes.data), "dfuse_kf_download")
+        return (FusionState(ld, scale.value, it.value), SemiDenseMap(sd, sv, valid, cnt.value),
+                mask)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().dfuse_kf_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

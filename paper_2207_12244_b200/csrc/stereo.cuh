@@ -1,0 +1,51 @@
+// stereo.cuh -- launch interface of the stereo front end (stereo.cu)
+#pragma once
+
+#include "common.cuh"
+
+namespace dfuse_cuda {
+
+struct SearchResult {
+  int status;
+  int best;
+  int n_steps;
+  dfuse_obs obs;
+};
+
+struct StereoArgs {
+  dfuse_epigeom g;
+  dfuse_search_cfg cfg;
+  const float* I0;
+  const float* I1;
+  int n_items;
+  int* work_counter;
+  // scan mode: masked-pixel list + semi map (in/out)
+  const int* list;
+  double* depth;
+  double* variance;
+  uint8_t* valid;
+  int* n_obs;
+  int* n_installed;
+  // list mode: pixels and optional priors
+  const double* px;
+  const double* prior;
+  const uint8_t* has_prior;
+  // optional outputs (slot = raster index in scan mode, item in list mode)
+  void* status;  // int8 (scan) / int32 (list)
+  int32_t* best;
+  int32_t* n_steps;
+  dfuse_obs* obs;
+  uint8_t* obs_flag;
+};
+
+void launch_texture_mask(dfuse_ctx* ctx, const float* img, int w, int h, double threshold,
+                         uint8_t* mask);
+void launch_mask_list(dfuse_ctx* ctx, const uint8_t* mask, long P, int* list, int* count);
+void launch_stereo(dfuse_ctx* ctx, const StereoArgs& a, bool list_mode);
+void launch_count_valid(dfuse_ctx* ctx, const uint8_t* valid, long P, int* out);
+void launch_compact_obs(dfuse_ctx* ctx, const uint8_t* flag, const dfuse_obs* dense, long P,
+                        int* block_scratch, dfuse_obs* out);
+void launch_update_list(dfuse_ctx* ctx, const dfuse_obs* obs, int n, int w, int h, int* head,
+                        int* link, int* bad, double* depth, double* variance, uint8_t* valid);
+
+}  // namespace dfuse_cuda

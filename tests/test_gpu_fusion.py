@@ -1,0 +1,181 @@
+"""GPU parity: the fusion optimiser (fusion.hpp) against the oracle.
+
+Tolerances (BASELINE.json north_star: "fused depth and variance within 1e-4
+relative after the fixed iteration count"): the GPU reduces in trees where
+the reference sums sequentially and CUDA's log/exp may differ from glibc's by
+an ulp, so
+  - per-pixel outputs of one sweep (assembly, gradient, SpMV): 1e-12 rel,
+  - reductions (cost, scale step): 1e-10 rel,
+  - PCG solutions: 1e-6 of max|delta| (the reference's own dense-solve bar,
+    test_fusion.cpp:127-142) and the iteration count within +-1,
+  - optimize: exp(log_depth) and scale within 1e-4 relative.
+"""
+import numpy as np
+import pytest
+
+from paper_2207_12244_b200 import synth
+from paper_2207_12244_b200._ffi import (DfuseError, FusionState, NormalEquations, RobustConfig,
+                                        SemiDenseMap, init_state)
+from helpers import (blank_problem, make_random_problem, quadratic_config, rel_err,
+                     semi_from_groundtruth, synth_oracle)
+
+pytestmark = pytest.mark.gpu
+MODES = ["full", "nopairwise", "lsscale"]
+
+
+def _problems():
+    yield make_random_problem(1, 8, 6)
+    yield make_random_problem(2, 33, 17, outlier_fraction=0.2)
+    yield make_random_problem(3, 1, 1)
+    yield make_random_problem(4, 1, 7)
+    yield make_random_problem(5, 9, 1)
+    yield make_random_problem(6, 257, 131, outlier_fraction=0.1)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_assemble_matches(gpu, orc, mode):
+    for st, semi, pred in _problems():
+        a = gpu.assemble_normal_equations(st, semi, pred, RobustConfig(), mode)
+        b = orc.assemble_normal_equations(st, semi, pred, RobustConfig(), mode)
+        for f in ("diag", "right", "down", "b"):
+            x, y = getattr(a, f), getattr(b, f)
+            assert np.allclose(x, y, rtol=1e-12, atol=1e-12 * np.abs(y).max()), f
+        if mode == "nopairwise":  # test_fusion.cpp:354-359
+            assert not a.right.any() and not a.down.any()
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_cost_and_gradient_match(gpu, orc, mode):
+    for st, semi, pred in _problems():
+        cg = gpu.total_cost(st, semi, pred, RobustConfig(), mode)
+        co = orc.total_cost(st, semi, pred, RobustConfig(), mode)
+        assert rel_err(cg, co) < 1e-10
+        c1, g1, s1 = gpu.cost_gradient(st, semi, pred, RobustConfig(), mode)
+        c2, g2, s2 = orc.cost_gradient(st, semi, pred, RobustConfig(), mode)
+        assert rel_err(c1, c2) < 1e-10
+        assert np.allclose(g1, g2, rtol=1e-12, atol=1e-12 * max(1.0, np.abs(g2).max()))
+        assert abs(s1 - s2) <= 1e-10 * max(1.0, abs(s2))
+
+
+def test_stencil_apply_bit_exact(gpu, orc):
+    rng = np.random.default_rng(0)
+    for (h, w) in [(1, 1), (3, 5), (64, 80), (480, 640)]:
+        eq = NormalEquations(*[rng.normal(size=(h, w)) for _ in range(4)])
+        x = rng.normal(size=(h, w))
+        assert gpu.stencil_apply(eq, x).tobytes() == orc.stencil_apply(eq, x).tobytes()
+
+
+def test_pcg_matches_oracle(gpu, orc):
+    for st, semi, pred in _problems():
+        cfg = RobustConfig(cg_tol=1e-10, cg_max_iters=500)
+        eq = orc.assemble_normal_equations(st, semi, pred, cfg, "full")
+        dg, ig = gpu.solve_depth_step(eq, cfg)
+        do, io = orc.solve_depth_step(eq, cfg)
+        scale = max(1.0, np.abs(do).max())
+        assert np.abs(dg - do).max() / scale < 1e-6
+        assert abs(ig - io) <= 1
+
+
+def test_pcg_zero_rhs_and_divergence(gpu):  # test_fusion.cpp:120-125, 400-411
+    st, semi, pred = blank_problem(3, 3)
+    eq = gpu.assemble_normal_equations(st, semi, pred)
+    d, its = gpu.solve_depth_step(eq)
+    assert not d.any() and its == 0
+    eq = NormalEquations(np.array([[1.0, 0.0], [1.0, 1.0]]), np.zeros((2, 2)), np.zeros((2, 2)),
+                         np.ones((2, 2)))
+    with pytest.raises(DfuseError) as e:
+        gpu.solve_depth_step(eq)
+    assert e.value.code == "CgDivergence"
+
+
+def test_scale_step(gpu, orc):  # test_fusion.cpp:162-196
+    cfg = RobustConfig(delta_semi=10.0)
+    st, semi, pred = blank_problem(2, 1)
+    semi.valid[:] = 1
+    semi.inlier_count = 2
+    semi.depth[:] = 1.0
+    semi.variance[0, 0], semi.variance[0, 1] = 1.0, 1.0 / 3.0
+    st.log_depth[0, 0] = np.log(2.0)
+    s = gpu.solve_scale_step(st, semi, cfg)
+    assert abs(s - np.exp(np.log(2.0) / 4.0)) < 1e-12 * s
+    with pytest.raises(DfuseError) as e:
+        gpu.solve_scale_step(st, SemiDenseMap.empty(2, 1), cfg)
+    assert e.value.code == "NoSemiDenseSupport"
+    for st, semi, pred in _problems():
+        if semi.inlier_count == 0:
+            continue
+        assert rel_err(gpu.solve_scale_step(st, semi), orc.solve_scale_step(st, semi)) < 1e-10
+
+
+def _check_opt(a, b, tol=1e-4):
+    assert a.iteration == b.iteration
+    assert rel_err(np.exp(a.log_depth), np.exp(b.log_depth)) < tol
+    assert rel_err(a.scale, b.scale) < tol
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_optimize_random_problems(gpu, orc, mode):
+    for st, semi, pred in _problems():
+        a, sa = gpu.optimize(st, semi, pred, RobustConfig(), mode, with_stats=True)
+        b, sb = orc.optimize(st, semi, pred, RobustConfig(), mode, with_stats=True)
+        _check_opt(a, b)
+        assert all(abs(x - y) <= 1 for x, y in zip(sa.pcg_iters, sb.pcg_iters))
+
+
+def test_optimize_kats(gpu):
+    # test_fusion.cpp:85-99: anchored 1x2 chain
+    st, semi, pred = blank_problem(2, 1)
+    pred.log_depth[0, 0] = 0.4
+    pred.log_depth_var[0, 0] = 1e-10
+    pred.log_depth_var[0, 1] = 1e12
+    pred.grad_x[0, 0] = np.log(2.0)
+    cfg = quadratic_config()
+    cfg.gn_iterations, cfg.estimate_scale = 3, False
+    out = gpu.optimize(st, semi, pred, cfg)
+    assert abs(out.log_depth[0, 0] - 0.4) < 1e-8
+    assert abs(out.log_depth[0, 1] - (0.4 + np.log(2.0))) < 1e-6
+    # test_fusion.cpp:226-239: single pixel splits the difference
+    st, semi, pred = blank_problem(1, 1)
+    semi.valid[:], semi.depth[:], semi.variance[:], semi.inlier_count = 1, 1.0, 1.0, 1
+    pred.log_depth[:] = 1.0
+    st.log_depth[:] = 1.0
+    cfg = quadratic_config()
+    cfg.estimate_scale, cfg.gn_iterations = False, 2
+    out = gpu.optimize(st, semi, pred, cfg)
+    assert abs(out.log_depth[0, 0] - 0.5) < 1e-9
+    # test_fusion.cpp:241-254: scale recovery
+    rng = np.random.default_rng(31)
+    gt = rng.uniform(1.0, 3.0, (12, 16))
+    pred = synth_oracle(gt, 0.05, 0.01, 77, 200.0)
+    semi = semi_from_groundtruth(gt, 0.5, 0.5, 0.05, 78)
+    out = gpu.optimize(init_state(pred), semi, pred, RobustConfig())
+    assert abs(out.scale - 2.0) < 0.05 * 2.0 and out.iteration == 10
+
+
+def test_optimize_transactional_on_divergence(gpu):
+    st, semi, pred = make_random_problem(9, 6, 5)
+    pred.log_depth_var[:] = -1.0  # negative information -> non-positive diagonal
+    pred.grad_x_var[:] = -1.0
+    pred.grad_y_var[:] = -1.0
+    semi.valid[:] = 0
+    semi.inlier_count = 0
+    with pytest.raises(DfuseError) as e:
+        gpu.optimize(st, semi, pred, RobustConfig())
+    assert e.value.code == "CgDivergence"
+
+
+@pytest.mark.parametrize("name", ["S", "C1"])
+def test_optimize_on_stereo_keyframe(gpu, orc, name):
+    spec = synth.small_spec(160, 120) if name == "S" else synth.CONFIGS["C1"]
+    seq = synth.make_sequence(spec, 8, frames=2)
+    mask = orc.texture_mask(seq.I0, 0.02)
+    semi = SemiDenseMap.empty(spec.width, spec.height)
+    st_o = init_state(seq.pred)
+    cfg = RobustConfig(gn_iterations=spec.gn_iterations)
+    for (q, t, I1) in seq.frames:
+        g = orc.make_epipolar_geometry(synth.IDENTITY_Q, np.zeros(3), q, t, spec.camera())
+        semi = orc.stereo_update(g, seq.I0, I1, mask, semi, spec.search).semi
+        st_g, sg = gpu.optimize(st_o, semi, seq.pred, cfg, with_stats=True)
+        st_o, so = orc.optimize(st_o, semi, seq.pred, cfg, with_stats=True)
+        _check_opt(st_g, st_o)
+        assert abs(sg.pcg_total - so.pcg_total) <= max(2, 0.02 * so.pcg_total)
