@@ -912,3 +912,77 @@ out:
   free(delta);
   return rc;
 }
+
+/* ------------------------------------------------------------------------
+ * KAT helpers */
+
+/* photometric_error_5pt, semidense.hpp:227-243 */
+int orc_photometric_error_5pt(const dfuse_epigeom* g, const float* I0, const float* I1, double x,
+                              double y, double d, double e[5]) {
+  double dx = g->K.fx * g->t_01[0] + (g->K.cx - x) * g->t_01[2];
+  double dy = g->K.fy * g->t_01[1] + (g->K.cy - y) * g->t_01[2];
+  const double n = sqrt(dx * dx + dy * dy);
+  if (n < 1e-12) {
+    dx = 1.0;
+    dy = 0.0;
+  } else {
+    dx = dx / n;
+    dy = dy / n;
+  }
+  stencil5 s;
+  if (!make_stencil(g, I0, x, y, dx, dy, &s)) return DFUSE_EPI_OUT_OF_BOUNDS;
+  switch (stencil_error(g, I1, &s, d, e)) {
+    case STEP_BEHIND: return DFUSE_EPI_BEHIND_CAMERA;
+    case STEP_OOB: return DFUSE_EPI_OUT_OF_BOUNDS;
+    default: break;
+  }
+  return DFUSE_EPI_OK;
+}
+
+/* jacobian_fd, semidense.hpp:253-261 */
+int orc_jacobian_fd(const double e_lo[5], const double e_hi[5], double d_lo, double d_hi,
+                    double J[5]) {
+  if (d_hi == d_lo) return DFUSE_E_ZERO_BASELINE_STEP;
+  const double inv = 1.0 / (d_hi - d_lo);
+  for (int j = 0; j < 5; ++j) J[j] = (e_hi[j] - e_lo[j]) * inv;
+  return DFUSE_OK;
+}
+
+/* observation_variance, semidense.hpp:267-272 */
+double orc_observation_variance(const double J[5]) {
+  double jtj = 0.0;
+  for (int j = 0; j < 5; ++j) jtj += J[j] * J[j];
+  if (jtj < 1e-12) return -1.0;
+  return 1.0 / jtj;
+}
+
+/* huber_weight / huber_cost, fusion.hpp:79-90 */
+int orc_huber(double r, double delta, double* weight, double* cost) {
+  int err = 0;
+  *weight = huber_weight(r, delta, &err);
+  *cost = huber_cost(r, delta);
+  return err;
+}
+
+/* residual_semi, fusion.hpp:51-53 */
+double orc_residual_semi(double ln_d, double s, double d_semi) {
+  return ln_d - log(s) - log(d_semi);
+}
+
+double orc_semi_log_variance(double variance, double depth) {
+  return semi_log_variance(variance, depth);
+}
+
+/* should_create_keyframe, semidense.hpp:419-424 */
+int orc_should_create_keyframe(const double q_kf[4], const double t_kf[3], const double q_cur[4],
+                               const double t_cur[3], double median, int inlier_count,
+                               double lambda_trans, int lambda_inliers, int* out) {
+  if (median <= 0.0) return DFUSE_E_NON_POSITIVE_DEPTH;
+  pose a = {{q_kf[0], q_kf[1], q_kf[2], q_kf[3]}, {t_kf[0], t_kf[1], t_kf[2]}};
+  pose b = {{q_cur[0], q_cur[1], q_cur[2], q_cur[3]}, {t_cur[0], t_cur[1], t_cur[2]}};
+  const pose rel = pose_compose(pose_inverse(a), b);
+  const double trans =
+      sqrt((rel.t[0] * rel.t[0] + rel.t[1] * rel.t[1]) + rel.t[2] * rel.t[2]);
+  *out = trans / median > lambda_trans || inlier_count < lambda_inliers;
+  return DFUSE_OK;
+}

@@ -63,6 +63,25 @@ extern "C" {
 DFUSE_ORACLE_DECLS(orc_)
 DFUSE_ORACLE_DECLS(ref_)
 
+/* small helpers the reference exposes for its KATs (semidense.hpp:227-272,
+ * fusion.hpp:51-100); same signatures under both prefixes */
+#define DFUSE_ORACLE_HELPERS(P)                                                                   \
+  int P##photometric_error_5pt(const dfuse_epigeom* g, const float* I0, const float* I1,         \
+                               double x, double y, double d, double e[5]);                       \
+  int P##jacobian_fd(const double e_lo[5], const double e_hi[5], double d_lo, double d_hi,      \
+                     double J[5]);                                                               \
+  double P##observation_variance(const double J[5]);                                             \
+  int P##huber(double r, double delta, double* weight, double* cost);                           \
+  double P##residual_semi(double ln_d, double s, double d_semi);                                 \
+  double P##semi_log_variance(double variance, double depth);                                    \
+  int P##should_create_keyframe(const double q_kf[4], const double t_kf[3],                     \
+                                const double q_cur[4], const double t_cur[3], double median,    \
+                                int inlier_count, double lambda_trans, int lambda_inliers,      \
+                                int* out);
+DFUSE_ORACLE_HELPERS(orc_)
+DFUSE_ORACLE_HELPERS(ref_)
+double orc_hypot(double x, double y);
+
 /* ref_ only: one tracked frame through the reference's process_frame
  * (pipeline.hpp:194-228) with retirement disabled, timed per stage like
  * StageTimer (pipeline.hpp:101-115). Returns the optimize error code (the

@@ -447,4 +447,70 @@ int ref_process_frame(const dfuse_epigeom* g, const float* I0, const float* I1,
   }
 }
 
+
+int ref_photometric_error_5pt(const dfuse_epigeom* g, const float* I0, const float* I1, double x,
+                              double y, double d, double e[5]) {
+  std::array<double, 5> ee{};
+  const EpipolarStatus st = photometric_error_5pt(make_geom(*g), make_image(I0, g->K.width, g->K.height),
+                                                  make_image(I1, g->K.width, g->K.height),
+                                                  PixelCoord{x, y}, d, ee);
+  for (int j = 0; j < 5; ++j) e[j] = ee[j];
+  return static_cast<int>(st);
+}
+
+int ref_jacobian_fd(const double e_lo[5], const double e_hi[5], double d_lo, double d_hi,
+                    double J[5]) {
+  try {
+    std::array<double, 5> a, b;
+    for (int j = 0; j < 5; ++j) {
+      a[j] = e_lo[j];
+      b[j] = e_hi[j];
+    }
+    const std::array<double, 5> r = jacobian_fd(a, b, d_lo, d_hi);
+    for (int j = 0; j < 5; ++j) J[j] = r[j];
+    return DFUSE_OK;
+  } catch (const Error& e) {
+    return code_of(e);
+  }
+}
+
+double ref_observation_variance(const double J[5]) {
+  std::array<double, 5> a;
+  for (int j = 0; j < 5; ++j) a[j] = J[j];
+  return observation_variance(a);
+}
+
+int ref_huber(double r, double delta, double* weight, double* cost) {
+  *cost = huber_cost(r, delta);
+  try {
+    *weight = huber_weight(r, delta);
+    return DFUSE_OK;
+  } catch (const Error& e) {
+    *weight = 0.0;
+    return code_of(e);
+  }
+}
+
+double ref_residual_semi(double ln_d, double s, double d_semi) {
+  return residual_semi(ln_d, s, d_semi);
+}
+
+double ref_semi_log_variance(double variance, double depth) {
+  return semi_log_variance(variance, depth);
+}
+
+int ref_should_create_keyframe(const double q_kf[4], const double t_kf[3], const double q_cur[4],
+                               const double t_cur[3], double median, int inlier_count,
+                               double lambda_trans, int lambda_inliers, int* out) {
+  try {
+    SemiDenseMap m;
+    m.inlier_count = inlier_count;
+    *out = should_create_keyframe(make_pose(q_kf, t_kf), make_pose(q_cur, t_cur), median, m,
+                                  KeyframePolicy{lambda_trans, lambda_inliers});
+    return DFUSE_OK;
+  } catch (const Error& e) {
+    return code_of(e);
+  }
+}
+
 }  // extern "C"
