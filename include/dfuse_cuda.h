@@ -150,6 +150,9 @@ int dfuse_ctx_destroy(dfuse_ctx* ctx);
 const char* dfuse_last_error(const dfuse_ctx* ctx);
 /* number of persistent CTAs the fusion solver uses (0 = one per SM) */
 int dfuse_ctx_set_solver_ctas(dfuse_ctx* ctx, int ctas);
+/* PCG data path: 0 = auto (SM-resident tiles when the raster fits on chip,
+ * else streaming from L2/HBM), 1 = always streaming */
+int dfuse_ctx_set_solver_path(dfuse_ctx* ctx, int path);
 /* kernels launched on this context since creation (evidence counter) */
 int64_t dfuse_ctx_launch_count(const dfuse_ctx* ctx);
 /* the context's cudaStream_t (for timing with events on the launch stream) */

@@ -76,6 +76,15 @@ class Context:
     def set_solver_ctas(self, n: int) -> None:
         lib().dfuse_ctx_set_solver_ctas(self.handle, int(n))
 
+    def set_solver_path(self, streaming: bool) -> None:
+        """False: SM-resident PCG when the raster fits on chip (default);
+        True: always the streaming PCG."""
+        L = lib()
+        L.dfuse_ctx_set_solver_path.argtypes = [C.c_void_p, C.c_int]
+        rc = L.dfuse_ctx_set_solver_path(self.handle, 1 if streaming else 0)
+        if rc:
+            raise DfuseError(rc, "dfuse_ctx_set_solver_path")
+
     def stream_handle(self) -> int:
         """cudaStream_t the library launches on (wrap with torch.cuda.ExternalStream)."""
         return int(lib().dfuse_ctx_stream(self.handle))

@@ -119,8 +119,7 @@ struct FusionWS {
   uint8_t* svalid;
   double* ld[2];
   double *diag, *right, *down, *b, *x, *r, *p0, *p1, *q;
-  double* partials;
-  unsigned* barrier;
+  ReduceSlot* slots;
   FusionControl* ctl;
   FusionStateDev* st;  // [2]
 };
@@ -129,8 +128,8 @@ size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 
 FusionWS alloc_fusion_ws(dfuse_ctx* ctx, long P, int grid, int slot) {
   const size_t dP = align_up(sizeof(double) * P);
-  size_t total = 6 * dP + 2 * dP + align_up(P) + 11 * dP + align_up(sizeof(double) * 8 * grid) +
-                 256 + align_up(sizeof(FusionControl)) + align_up(2 * sizeof(FusionStateDev));
+  size_t total = 6 * dP + 2 * dP + align_up(P) + 11 * dP + align_up(fusion_slots_bytes(grid)) +
+                 align_up(sizeof(FusionControl)) + align_up(2 * sizeof(FusionStateDev));
   char* base = (char*)scratch(ctx, slot, total);
   FusionWS w;
   size_t o = 0;
@@ -154,8 +153,8 @@ FusionWS alloc_fusion_ws(dfuse_ctx* ctx, long P, int grid, int slot) {
   w.p0 = (double*)take(dP);
   w.p1 = (double*)take(dP);
   w.q = (double*)take(dP);
-  w.partials = (double*)take(sizeof(double) * 8 * grid);
-  w.barrier = (unsigned*)take(256);
+  w.slots = (ReduceSlot*)take(fusion_slots_bytes(grid));
+  DF_CUDA(cudaMemsetAsync(w.slots, 0, fusion_slots_bytes(grid), ctx->stream));
   w.ctl = (FusionControl*)take(sizeof(FusionControl));
   w.st = (FusionStateDev*)take(2 * sizeof(FusionStateDev));
   return w;
@@ -181,8 +180,7 @@ void fill_args(FusionArgs& a, const FusionWS& w, int W, int H) {
   a.p[0] = w.p0;
   a.p[1] = w.p1;
   a.q = w.q;
-  a.partials = w.partials;
-  a.barrier = w.barrier;
+  a.slots = w.slots;
   a.ctl = w.ctl;
   a.st_in = w.st;
   a.st_out = w.st + 1;
@@ -283,6 +281,12 @@ const char* dfuse_last_error(const dfuse_ctx* ctx) {
 int dfuse_ctx_set_solver_ctas(dfuse_ctx* ctx, int ctas) {
   if (!ctx || ctas < 0) return DFUSE_E_INVALID_ARGUMENT;
   ctx->solver_ctas = ctas;
+  return DFUSE_OK;
+}
+
+int dfuse_ctx_set_solver_path(dfuse_ctx* ctx, int path) {
+  if (!ctx || path < 0 || path > 1) return DFUSE_E_INVALID_ARGUMENT;
+  ctx->force_streaming = path;
   return DFUSE_OK;
 }
 

@@ -30,6 +30,7 @@ struct dfuse_ctx {
   int device = 0;
   int num_sms = 0;
   int solver_ctas = 0;  // 0 = auto (one per SM)
+  int force_streaming = 0;  // 1: never use the SM-resident PCG
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {};
   std::string last_error;

@@ -62,40 +62,34 @@ __device__ __forceinline__ double semi_logvar(double v, double d) {  // fusion.h
 }
 
 // ---------------------------------------------------------------------------
-// grid barrier + deterministic all-reduce
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+// Grid-wide deterministic all-reduce without atomics. Every CTA publishes
+// its partial sums in its own 64-byte slot with a release store of a tag
+// (launch id + phase); every CTA's warp 0 polls all slots with acquire loads
+// and sums them in a fixed order, so all CTAs get identical bits. Slots are
+// double-buffered by phase parity: a CTA can run at most one phase ahead of
+// the slowest reader. No counter is shared, so nothing serialises on one L2
+// address (hard part 3: the PCG needs 2 of these per iteration).
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 struct GridCtx {
-  unsigned* arrive;
-  double* partials;  // [2][G][4]
+  ReduceSlot* slots;  // [2][G]
   unsigned G;
-  unsigned epoch;
+  unsigned long long base_tag;
   unsigned phase;
   int syncs;
 };
 
-__device__ __forceinline__ void grid_sync(GridCtx& c) {
-  __syncthreads();
-  c.epoch += 1;
-  c.syncs += 1;
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(c.arrive, 1u);
-    const unsigned target = c.epoch * c.G;
-    while (ld_acquire(c.arrive) < target) {
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 // Sum v[0..NV) over every thread of the grid. Order: per-thread sequential
 // partials (caller) -> warp butterfly -> CTA (warp 0 over warp partials) ->
-// fixed-order sum over the G CTA partials. Identical result in every thread.
+// per-lane strided sums over the G CTA slots -> warp butterfly. Identical
+// result in every thread of every CTA. Doubles as the grid barrier.
 template <int NV>
 __device__ void grid_allreduce(GridCtx& c, double (&v)[NV]) {
   __shared__ double red[FW][4];
@@ -107,29 +101,43 @@ __device__ void grid_allreduce(GridCtx& c, double (&v)[NV]) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) red[wid][k] = v[k];
   __syncthreads();
-  double* part = c.partials + (size_t)(c.phase & 1) * c.G * 4;
   if (wid == 0) {
+    const unsigned long long tag = c.base_tag + c.phase + 1;
+    ReduceSlot* buf = c.slots + (size_t)(c.phase & 1) * c.G;
+    double t[NV > 0 ? NV : 1];
 #pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      double t = lane < FW ? red[lane][k] : 0.0;
-      t = warp_sum(t);
-      if (lane == 0) part[(size_t)blockIdx.x * 4 + k] = t;
-    }
-  }
-  grid_sync(c);
-  if (wid == 0) {
+    for (int k = 0; k < NV; ++k) t[k] = warp_sum(lane < FW ? red[lane][k] : 0.0);
+    if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      double t = 0.0;
-      for (unsigned b = lane; b < c.G; b += 32) t += __ldcg(part + (size_t)b * 4 + k);
-      t = warp_sum(t);
-      if (lane == 0) bcast[k] = t;
+      for (int k = 0; k < NV; ++k) buf[blockIdx.x].v[k] = t[k];
+      st_release_u64(&buf[blockIdx.x].tag, tag);
     }
+    double acc[NV > 0 ? NV : 1];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+    for (unsigned b = lane; b < c.G; b += 32) {
+      while (ld_acquire_u64(&buf[b].tag) != tag) {
+      }
+#pragma unroll
+      for (int k = 0; k < NV; ++k) acc[k] += __ldcg(&buf[b].v[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] = warp_sum(acc[k]);
+    __threadfence();
+    if (lane == 0)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) bcast[k] = acc[k];
   }
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < NV; ++k) v[k] = bcast[k];
   c.phase += 1;
+  c.syncs += 1;
+}
+
+__device__ __forceinline__ void grid_sync(GridCtx& c) {
+  double none[1] = {0.0};
+  grid_allreduce(c, none);
 }
 
 // ---------------------------------------------------------------------------
@@ -388,8 +396,201 @@ __device__ int pcg_loop(GridCtx& c, const FusionArgs& a, const Range& rg, double
 }
 
 // ---------------------------------------------------------------------------
+// SM-resident Jacobi PCG (same iteration as pcg_loop, same stop rules).
+// CTA b owns tile b of a tiles_x x tiles_y partition of the raster. For the
+// whole solve its x and r live in registers (PPT pixels per thread), diag /
+// right / down and p (with a one-pixel halo) in shared memory. Per iteration
+// only the tile boundary leaves the SM: each CTA publishes its boundary p
+// (sweep A, parity buffer) and r (sweep B) into the raster arrays in L2, and
+// rebuilds the halo as p = r/diag + beta p_prev from the neighbours'
+// published values -- the same expression the owner evaluates, so halo and
+// owner values are bit-identical and no extra barrier is needed. The two
+// grid all-reduces (p.q; r.r and r.z) are the only synchronisation.
+struct TileGeo {
+  int x0, y0, tw, th;  // tw*th == 0 for CTAs without a tile
+};
+
+__device__ __forceinline__ TileGeo my_tile(const FusionArgs& a) {
+  TileGeo t{0, 0, 0, 0};
+  const int nt = a.tiles_x * a.tiles_y;
+  if ((int)blockIdx.x < nt) {
+    const int bx = blockIdx.x % a.tiles_x, by = blockIdx.x / a.tiles_x;
+    t.x0 = (int)((long)a.W * bx / a.tiles_x);
+    t.y0 = (int)((long)a.H * by / a.tiles_y);
+    t.tw = (int)((long)a.W * (bx + 1) / a.tiles_x) - t.x0;
+    t.th = (int)((long)a.H * (by + 1) / a.tiles_y) - t.y0;
+  }
+  return t;
+}
+
+template <int PPT>
+__device__ int pcg_resident(GridCtx& c, const FusionArgs& a, double bnorm2, double rz, int* its) {
+  extern __shared__ double dsm[];
+  const TileGeo tg = my_tile(a);
+  const int T = tg.tw * tg.th;
+  const int TC = PPT * FT;  // tile capacity
+  double* s_diag = dsm;
+  double* s_right = dsm + TC;
+  double* s_down = dsm + 2 * TC;
+  double* s_p = dsm + 3 * TC;                        // (th+2) x (tw+2), halo included
+  double* s_hright = s_p + (a.th_max + 2) * (a.tw_max + 2);  // right[] of the left halo column
+  double* s_hdown = s_hright + a.th_max;                      // down[] of the top halo row
+  const int W = a.W, H = a.H, pw = tg.tw + 2;
+  const int ring_n = T > 0 ? 2 * (tg.tw + tg.th) : 0;
+
+  double xr[PPT], rr_[PPT], qr[PPT];
+  int gi_[PPT];  // global pixel index, -1 if none
+#pragma unroll
+  for (int j = 0; j < PPT; ++j) {
+    const int k = threadIdx.x + FT * j;
+    xr[j] = 0.0;
+    qr[j] = 0.0;
+    rr_[j] = 0.0;
+    gi_[j] = -1;
+    if (k < T) {
+      const int ly = k / tg.tw, lx = k - ly * tg.tw;
+      const int gi = (tg.y0 + ly) * W + tg.x0 + lx;
+      gi_[j] = gi;
+      s_diag[k] = __ldcg(a.diag + gi);
+      s_right[k] = __ldcg(a.right + gi);
+      s_down[k] = __ldcg(a.down + gi);
+      rr_[j] = __ldcg(a.r + gi);
+    }
+  }
+  for (int t = threadIdx.x; t < tg.th; t += FT)
+    s_hright[t] = tg.x0 > 0 ? __ldcg(a.right + (tg.y0 + t) * W + tg.x0 - 1) : 0.0;
+  for (int t = threadIdx.x; t < tg.tw; t += FT)
+    s_hdown[t] = tg.y0 > 0 ? __ldcg(a.down + (tg.y0 - 1) * W + tg.x0 + t) : 0.0;
+  __syncthreads();
+
+  const double tol2 = a.cg_tol * a.cg_tol * bnorm2;
+  double prev = bnorm2, beta = 0.0;
+  int streak = 0, status = 0;
+  *its = 0;
+  for (int it = 0; it < a.cg_max; ++it) {
+    *its = it + 1;
+    const bool first = it == 0;
+    const double* pprev_g = a.p[(it + 1) & 1];
+    double* pcur_g = a.p[it & 1];
+    // ---- sweep A: halo ring from the neighbours' published r, p_prev
+    if ((int)threadIdx.x < ring_n) {
+      const int t = threadIdx.x;
+      int gx, gy, so;
+      if (t < tg.tw) {
+        gx = tg.x0 + t, gy = tg.y0 - 1, so = t + 1;
+      } else if (t < 2 * tg.tw) {
+        gx = tg.x0 + t - tg.tw, gy = tg.y0 + tg.th, so = (tg.th + 1) * pw + t - tg.tw + 1;
+      } else if (t < 2 * tg.tw + tg.th) {
+        gx = tg.x0 - 1, gy = tg.y0 + t - 2 * tg.tw, so = (t - 2 * tg.tw + 1) * pw;
+      } else {
+        gx = tg.x0 + tg.tw, gy = tg.y0 + t - 2 * tg.tw - tg.th,
+        so = (t - 2 * tg.tw - tg.th + 1) * pw + tg.tw + 1;
+      }
+      if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
+        const int j = gy * W + gx;
+        const double z = __ldcg(a.r + j) / __ldcg(a.diag + j);
+        s_p[so] = first ? z : z + beta * __ldcg(pprev_g + j);
+      }
+    }
+    // own p = z + beta p (fusion.hpp:360,365; p = z at it 0, fusion.hpp:329-330)
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      const int k = threadIdx.x + FT * j;
+      if (k < T) {
+        const int ly = k / tg.tw, lx = k - ly * tg.tw;
+        const int so = (ly + 1) * pw + lx + 1;
+        const double z = rr_[j] / s_diag[k];
+        const double p = first ? z : z + beta * s_p[so];
+        s_p[so] = p;
+        if (lx == 0 || ly == 0 || lx == tg.tw - 1 || ly == tg.th - 1) pcur_g[gi_[j]] = p;
+      }
+    }
+    __syncthreads();
+    // q = H p, StencilMatrix::apply order (fusion.hpp:127-131)
+    double pq = 0.0;
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      const int k = threadIdx.x + FT * j;
+      if (k < T) {
+        const int ly = k / tg.tw, lx = k - ly * tg.tw;
+        const int so = (ly + 1) * pw + lx + 1;
+        const int gx = tg.x0 + lx, gy = tg.y0 + ly;
+        const double pi = s_p[so];
+        double v = s_diag[k] * pi;
+        if (gx + 1 < W) v += s_right[k] * s_p[so + 1];
+        if (gx > 0) v += (lx > 0 ? s_right[k - 1] : s_hright[ly]) * s_p[so - 1];
+        if (gy + 1 < H) v += s_down[k] * s_p[so + pw];
+        if (gy > 0) v += (ly > 0 ? s_down[k - tg.tw] : s_hdown[lx]) * s_p[so - pw];
+        qr[j] = v;
+        pq += pi * v;
+      }
+    }
+    double v1[1] = {pq};
+    grid_allreduce(c, v1);
+    if (!(v1[0] > 0.0)) {
+      status = DFUSE_E_CG_DIVERGENCE;
+      break;
+    }
+    const double alpha = rz / v1[0];
+    // ---- sweep B (fusion.hpp:345-362)
+    double rr = 0.0, rzn = 0.0;
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      const int k = threadIdx.x + FT * j;
+      if (k < T) {
+        const int ly = k / tg.tw, lx = k - ly * tg.tw;
+        const int so = (ly + 1) * pw + lx + 1;
+        xr[j] = xr[j] + alpha * s_p[so];
+        const double r = rr_[j] - alpha * qr[j];
+        rr_[j] = r;
+        rr += r * r;
+        rzn += r * (r / s_diag[k]);
+        if (lx == 0 || ly == 0 || lx == tg.tw - 1 || ly == tg.th - 1) a.r[gi_[j]] = r;
+      }
+    }
+    double v2[2] = {rr, rzn};
+    grid_allreduce(c, v2);
+    const double rn = v2[0];
+    if (rn <= tol2) break;
+    if (rn > prev) {
+      if (++streak >= 10) {
+        status = DFUSE_E_CG_DIVERGENCE;
+        break;
+      }
+    } else {
+      streak = 0;
+    }
+    prev = rn;
+    beta = v2[1] / rz;
+    rz = v2[1];
+  }
+  // delta to the raster for the line search (x == 0 if no iteration ran)
+#pragma unroll
+  for (int j = 0; j < PPT; ++j)
+    if (gi_[j] >= 0) a.x[gi_[j]] = xr[j];
+  grid_sync(c);
+  return status;
+}
+
+template <int PPT>
+__device__ __forceinline__ int pcg_solve(GridCtx& c, const FusionArgs& a, const Range& rg,
+                                         double bnorm2, double rz, int* its) {
+  if constexpr (PPT > 0) {
+    return pcg_resident<PPT>(c, a, bnorm2, rz, its);
+  } else {
+    const int st = pcg_loop(c, a, rg, bnorm2, rz, its);
+    if (*its == 0) {
+      sweep_zero_x(a, rg);
+      grid_sync(c);
+    }
+    return st;
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <int PPT>
 __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
-  GridCtx c{a.barrier, a.partials, gridDim.x, 0u, 0u, 0};
+  GridCtx c{a.slots, gridDim.x, a.base_tag, 0u, 0};
   const Range rg = my_range(a);
   const Sel sel = terms_for(a.mode);
   FusionControl* ctl = a.ctl;
@@ -433,8 +634,7 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
     } else if (w[2] > 0.0) {
       status = DFUSE_E_CG_DIVERGENCE;
     } else {
-      status = pcg_loop(c, a, rg, w[0], w[1], &its);
-      if (its == 0) sweep_zero_x(a, rg);
+      status = pcg_solve<PPT>(c, a, rg, w[0], w[1], &its);
     }
     if (leader) ctl->pcg_last = its;
   } else {  // OP_OPTIMIZE, fusion.hpp:402-454
@@ -496,7 +696,7 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
           if (v[2] > 0.0) {
             status = DFUSE_E_CG_DIVERGENCE;
           } else {
-            status = pcg_loop(c, a, rg, v[0], v[1], &its);
+            status = pcg_solve<PPT>(c, a, rg, v[0], v[1], &its);
           }
         }
         pcg_total += its;
@@ -560,7 +760,7 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
 // i receives, in the reference's order: +d_y of i-W, +d_x of i-1, net,
 // semi, -d_x of i, -d_y of i. Cost and d/d ln s are grid reductions.
 __global__ void __launch_bounds__(FT, 1) k_gradient(FusionArgs a, double* g) {
-  GridCtx c{a.barrier, a.partials, gridDim.x, 0u, 0u, 0};
+  GridCtx c{a.slots, gridDim.x, a.base_tag, 0u, 0};
   const Range rg = my_range(a);
   const Sel sel = terms_for(a.mode);
   const double ln_s = sel.scale ? log(a.scale0) : 0.0;
@@ -631,30 +831,95 @@ __global__ void k_stencil_apply(int W, int H, const double* __restrict__ diag,
 }
 
 // ---------------------------------------------------------------------------
+static unsigned long long next_tag() {
+  static unsigned long long seq = 0;  // host-side launch sequence (one process)
+  return (__atomic_add_fetch(&seq, 1ULL, __ATOMIC_RELAXED)) << 32;
+}
+
+template <int PPT>
+static size_t resident_smem(int tw_max, int th_max) {
+  return sizeof(double) * ((size_t)3 * PPT * FT + (size_t)(th_max + 2) * (tw_max + 2) + th_max +
+                           tw_max);
+}
+
 int fusion_grid(dfuse_ctx* ctx) {
   static int occ = -1;
   if (occ < 0) {
-    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fusion, FT, 0));
-    int occ2 = 0;
-    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_gradient, FT, 0));
-    if (occ2 < occ) occ = occ2;
+    int o0 = 0, o4 = 0, o8 = 0, og = 0;
+    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o0, k_fusion<0>, FT, 0));
+    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o4, k_fusion<4>, FT, 0));
+    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o8, k_fusion<8>, FT, 0));
+    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&og, k_gradient, FT, 0));
+    occ = o0;
+    if (o4 < occ) occ = o4;
+    if (o8 < occ) occ = o8;
+    if (og < occ) occ = og;
     if (occ < 1) throw CudaFailure{cudaErrorLaunchOutOfResources, "k_fusion occupancy"};
   }
   int g = ctx->solver_ctas > 0 ? ctx->solver_ctas : ctx->num_sms;
-  if (g > ctx->num_sms * occ) g = ctx->num_sms * occ;
+  if (g > ctx->num_sms) g = ctx->num_sms;  // one CTA per SM: resident tiles need the SM's smem
   return g;
 }
 
-void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
-  DF_CUDA(cudaMemsetAsync(a.barrier, 0, sizeof(unsigned), ctx->stream));
+size_t fusion_slots_bytes(int grid) { return sizeof(ReduceSlot) * 2 * (size_t)grid; }
+
+// tile partition for the resident PCG: tx x ty <= grid tiles, minimal
+// largest tile, then minimal halo
+void plan_tiles(FusionArgs& a, int grid) {
+  long best = -1;
+  int bx = 1, by = 1;
+  for (int tx = 1; tx <= grid && tx <= a.W; ++tx) {
+    int ty = grid / tx;
+    if (ty > a.H) ty = a.H;
+    if (ty < 1) break;
+    const long tw = (a.W + tx - 1) / tx, th = (a.H + ty - 1) / ty;
+    const long cost = tw * th * 64 + (tw + th);
+    if (best < 0 || cost < best) {
+      best = cost;
+      bx = tx;
+      by = ty;
+    }
+  }
+  a.tiles_x = bx;
+  a.tiles_y = by;
+  a.tw_max = (a.W + bx - 1) / bx;
+  a.th_max = (a.H + by - 1) / by;
+  const long T = (long)a.tw_max * a.th_max;
+  a.ppt = T <= 4L * FT ? 4 : (T <= 8L * FT ? 8 : 0);
+}
+
+template <int PPT>
+static void launch_fusion_t(dfuse_ctx* ctx, FusionArgs& a, int grid) {
+  size_t smem = 0;
+  if (PPT > 0) {
+    smem = resident_smem<PPT>(a.tw_max, a.th_max);
+    static size_t configured = 0;
+    if (smem > configured) {
+      DF_CUDA(cudaFuncSetAttribute((const void*)k_fusion<PPT>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      configured = smem;
+    }
+  }
   void* args[] = {&a};
-  DF_CUDA(cudaLaunchCooperativeKernel((const void*)k_fusion, dim3(grid), dim3(FT), args, 0,
-                                      ctx->stream));
+  DF_CUDA(cudaLaunchCooperativeKernel((const void*)k_fusion<PPT>, dim3(grid), dim3(FT), args,
+                                      smem, ctx->stream));
+}
+
+void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
+  plan_tiles(a, grid);
+  if (ctx->force_streaming) a.ppt = 0;
+  a.base_tag = next_tag();
+  if (a.ppt == 4)
+    launch_fusion_t<4>(ctx, a, grid);
+  else if (a.ppt == 8)
+    launch_fusion_t<8>(ctx, a, grid);
+  else
+    launch_fusion_t<0>(ctx, a, grid);
   DF_LAUNCHED(ctx);
 }
 
 void launch_gradient(dfuse_ctx* ctx, FusionArgs& a, int grid, double* g) {
-  DF_CUDA(cudaMemsetAsync(a.barrier, 0, sizeof(unsigned), ctx->stream));
+  a.base_tag = next_tag();
   void* args[] = {&a, &g};
   DF_CUDA(cudaLaunchCooperativeKernel((const void*)k_gradient, dim3(grid), dim3(FT), args, 0,
                                       ctx->stream));

@@ -15,6 +15,13 @@ struct FusionStateDev {
   int cur;
 };
 
+// one CTA's published partial sums for the grid all-reduce (fusion.cu)
+struct ReduceSlot {
+  double v[4];
+  unsigned long long tag;
+  unsigned long long pad[3];
+};
+
 struct FusionControl {
   int status;
   int ld_final;   // which ld buffer holds the result
@@ -48,12 +55,14 @@ struct FusionArgs {
   double* r;
   double* p[2];
   double* q;
-  double* partials;   // [2][grid][4]
-  unsigned* barrier;  // arrive counter (zeroed before each launch)
+  ReduceSlot* slots;  // [2][grid] all-reduce slots
+  unsigned long long base_tag;  // unique per launch (set by launch_*)
+  int tiles_x, tiles_y, tw_max, th_max, ppt;  // resident-PCG tiling (set by launch_fusion)
   FusionControl* ctl;
 };
 
 int fusion_grid(dfuse_ctx* ctx);
+size_t fusion_slots_bytes(int grid);
 void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid);
 void launch_gradient(dfuse_ctx* ctx, FusionArgs& a, int grid, double* g);
 void launch_stencil_apply(dfuse_ctx* ctx, int W, int H, const double* diag, const double* right,

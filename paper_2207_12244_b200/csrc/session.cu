@@ -170,8 +170,8 @@ int dfuse_kf_create(dfuse_ctx* ctx, const dfuse_intrinsics* K, const float* I0,
     kf->grid = fusion_grid(ctx);
     const size_t dP = al(sizeof(double) * P);
     const size_t total = 2 * al(sizeof(float) * P) + al(P) + al(sizeof(int) * P) + 2 * dP +
-                         al(P) + 256 + 6 * dP + 11 * dP + al(sizeof(double) * 8 * kf->grid) +
-                         256 + al(sizeof(FusionControl)) + al(2 * sizeof(FusionStateDev));
+                         al(P) + 256 + 6 * dP + 11 * dP + al(fusion_slots_bytes(kf->grid)) +
+                         al(sizeof(FusionControl)) + al(2 * sizeof(FusionStateDev));
     DF_CUDA(cudaMalloc(&kf->block, total));
     char* p = (char*)kf->block;
     auto take = [&](size_t bytes) {
@@ -207,8 +207,8 @@ int dfuse_kf_create(dfuse_ctx* ctx, const dfuse_intrinsics* K, const float* I0,
     f.p[0] = (double*)take(dP);
     f.p[1] = (double*)take(dP);
     f.q = (double*)take(dP);
-    f.partials = (double*)take(sizeof(double) * 8 * kf->grid);
-    f.barrier = (unsigned*)take(256);
+    f.slots = (ReduceSlot*)take(fusion_slots_bytes(kf->grid));
+    DF_CUDA(cudaMemsetAsync(f.slots, 0, fusion_slots_bytes(kf->grid), ctx->stream));
     f.ctl = (FusionControl*)take(sizeof(FusionControl));
     kf->st = (FusionStateDev*)take(2 * sizeof(FusionStateDev));
     DF_CUDA(cudaMallocHost(&kf->h_ctl, sizeof(FusionControl)));

@@ -23,6 +23,14 @@ pytestmark = pytest.mark.gpu
 MODES = ["full", "nopairwise", "lsscale"]
 
 
+@pytest.fixture(params=["resident", "streaming"], autouse=True)
+def solver_path(request, gpu_ctx):
+    """Every test runs on both PCG data paths (SM-resident tiles / streaming)."""
+    gpu_ctx.set_solver_path(request.param == "streaming")
+    yield request.param
+    gpu_ctx.set_solver_path(False)
+
+
 def _problems():
     yield make_random_problem(1, 8, 6)
     yield make_random_problem(2, 33, 17, outlier_fraction=0.2)
@@ -179,3 +187,16 @@ def test_optimize_on_stereo_keyframe(gpu, orc, name):
         st_o, so = orc.optimize(st_o, semi, seq.pred, cfg, with_stats=True)
         _check_opt(st_g, st_o)
         assert abs(sg.pcg_total - so.pcg_total) <= max(2, 0.02 * so.pcg_total)
+
+
+@pytest.mark.parametrize("shape", [(480, 640), (768, 1024)])
+def test_optimize_large_rasters(gpu, orc, shape):
+    """C2 size (resident tiles with 8 px/thread) and a raster too large for
+    the SM-resident path (auto-selects streaming)."""
+    h, w = shape
+    st, semi, pred = make_random_problem(77, w, h, outlier_fraction=0.05)
+    cfg = RobustConfig(gn_iterations=3)
+    a, sa = gpu.optimize(st, semi, pred, cfg, with_stats=True)
+    b, sb = orc.optimize(st, semi, pred, cfg, with_stats=True)
+    _check_opt(a, b)
+    assert all(abs(x - y) <= 1 for x, y in zip(sa.pcg_iters, sb.pcg_iters))
