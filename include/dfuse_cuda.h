@@ -155,6 +155,9 @@ int dfuse_ctx_set_solver_ctas(dfuse_ctx* ctx, int ctas);
 int dfuse_ctx_set_solver_path(dfuse_ctx* ctx, int path);
 /* kernels launched on this context since creation (evidence counter) */
 int64_t dfuse_ctx_launch_count(const dfuse_ctx* ctx);
+/* diagnostics: device time (ms) of one cooperative launch running n grid-wide
+ * all-reduces of the fusion solver on `grid` CTAs (variant 1 = production) */
+int dfuse_debug_sync_bench(dfuse_ctx* ctx, int n, int variant, int grid, float* ms);
 /* the context's cudaStream_t (for timing with events on the launch stream) */
 void* dfuse_ctx_stream(const dfuse_ctx* ctx);
 

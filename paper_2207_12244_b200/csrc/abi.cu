@@ -120,6 +120,7 @@ struct FusionWS {
   double* ld[2];
   double *diag, *right, *down, *b, *x, *r, *p0, *p1, *q;
   ReduceSlot* slots;
+  unsigned long long* halo;
   FusionControl* ctl;
   FusionStateDev* st;  // [2]
 };
@@ -128,8 +129,10 @@ size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 
 FusionWS alloc_fusion_ws(dfuse_ctx* ctx, long P, int grid, int slot) {
   const size_t dP = align_up(sizeof(double) * P);
+  const bool resident = fusion_resident_possible(P, grid);
   size_t total = 6 * dP + 2 * dP + align_up(P) + 11 * dP + align_up(fusion_slots_bytes(grid)) +
-                 align_up(sizeof(FusionControl)) + align_up(2 * sizeof(FusionStateDev));
+                 align_up(sizeof(FusionControl)) + align_up(2 * sizeof(FusionStateDev)) +
+                 (resident ? align_up(fusion_halo_bytes(P)) : 0);
   char* base = (char*)scratch(ctx, slot, total);
   FusionWS w;
   size_t o = 0;
@@ -154,9 +157,9 @@ FusionWS alloc_fusion_ws(dfuse_ctx* ctx, long P, int grid, int slot) {
   w.p1 = (double*)take(dP);
   w.q = (double*)take(dP);
   w.slots = (ReduceSlot*)take(fusion_slots_bytes(grid));
-  DF_CUDA(cudaMemsetAsync(w.slots, 0, fusion_slots_bytes(grid), ctx->stream));
   w.ctl = (FusionControl*)take(sizeof(FusionControl));
   w.st = (FusionStateDev*)take(2 * sizeof(FusionStateDev));
+  w.halo = resident ? (unsigned long long*)take(fusion_halo_bytes(P)) : nullptr;
   return w;
 }
 
@@ -181,6 +184,7 @@ void fill_args(FusionArgs& a, const FusionWS& w, int W, int H) {
   a.p[1] = w.p1;
   a.q = w.q;
   a.slots = w.slots;
+  a.halo = w.halo;
   a.ctl = w.ctl;
   a.st_in = w.st;
   a.st_out = w.st + 1;
@@ -250,6 +254,8 @@ int dfuse_ctx_create(int device, dfuse_ctx** out) {
   if (!ctx) return DFUSE_E_CUDA;
   ctx->device = device;
   ctx->num_sms = prop.multiProcessorCount;
+  const char* tr = getenv("DFUSE_TRACE");
+  ctx->trace = tr && tr[0] == '1';
   if (cudaSetDevice(device) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete ctx;
@@ -282,6 +288,13 @@ int dfuse_ctx_set_solver_ctas(dfuse_ctx* ctx, int ctas) {
   if (!ctx || ctas < 0) return DFUSE_E_INVALID_ARGUMENT;
   ctx->solver_ctas = ctas;
   return DFUSE_OK;
+}
+
+int dfuse_debug_sync_bench(dfuse_ctx* ctx, int n, int variant, int grid, float* ms) {
+  return guarded(ctx, [&] {
+    require(ms != nullptr && n >= 0, DFUSE_E_INVALID_ARGUMENT, "bad arguments");
+    *ms = sync_bench(ctx, n, variant, grid);
+  });
 }
 
 int dfuse_ctx_set_solver_path(dfuse_ctx* ctx, int path) {

@@ -31,6 +31,7 @@ struct dfuse_ctx {
   int num_sms = 0;
   int solver_ctas = 0;  // 0 = auto (one per SM)
   int force_streaming = 0;  // 1: never use the SM-resident PCG
+  int trace = 0;            // DFUSE_TRACE=1: print per-phase PCG cycle counts
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {};
   std::string last_error;

@@ -29,6 +29,7 @@ struct FusionControl {
   int pcg_last;
   double scale;
   double value[2];
+  long long trace[8];  // SM cycles per PCG phase, CTA 0 (DFUSE_TRACE=1)
   dfuse_solver_stats stats;
 };
 
@@ -55,14 +56,19 @@ struct FusionArgs {
   double* r;
   double* p[2];
   double* q;
-  ReduceSlot* slots;  // [2][grid] all-reduce slots
+  ReduceSlot* slots;  // [2][grid] all-reduce slots (+1)
   unsigned long long base_tag;  // unique per launch (set by launch_*)
+  unsigned long long* halo;     // resident PCG LL halo words [3][P][2], or null
   int tiles_x, tiles_y, tw_max, th_max, ppt;  // resident-PCG tiling (set by launch_fusion)
+  int trace;  // record per-phase cycle counts of the resident PCG in ctl->trace
   FusionControl* ctl;
 };
 
 int fusion_grid(dfuse_ctx* ctx);
 size_t fusion_slots_bytes(int grid);
+size_t fusion_halo_bytes(long P);
+bool fusion_resident_possible(long P, int grid);
+float sync_bench(dfuse_ctx* ctx, int n, int variant, int grid);
 void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid);
 void launch_gradient(dfuse_ctx* ctx, FusionArgs& a, int grid, double* g);
 void launch_stencil_apply(dfuse_ctx* ctx, int W, int H, const double* diag, const double* right,

@@ -169,9 +169,11 @@ int dfuse_kf_create(dfuse_ctx* ctx, const dfuse_intrinsics* K, const float* I0,
     const long P = kf->P = (long)kf->W * kf->H;
     kf->grid = fusion_grid(ctx);
     const size_t dP = al(sizeof(double) * P);
+    const bool resident = fusion_resident_possible(P, kf->grid);
     const size_t total = 2 * al(sizeof(float) * P) + al(P) + al(sizeof(int) * P) + 2 * dP +
                          al(P) + 256 + 6 * dP + 11 * dP + al(fusion_slots_bytes(kf->grid)) +
-                         al(sizeof(FusionControl)) + al(2 * sizeof(FusionStateDev));
+                         al(sizeof(FusionControl)) + al(2 * sizeof(FusionStateDev)) +
+                         (resident ? al(fusion_halo_bytes(P)) : 0);
     DF_CUDA(cudaMalloc(&kf->block, total));
     char* p = (char*)kf->block;
     auto take = [&](size_t bytes) {
@@ -208,7 +210,7 @@ int dfuse_kf_create(dfuse_ctx* ctx, const dfuse_intrinsics* K, const float* I0,
     f.p[1] = (double*)take(dP);
     f.q = (double*)take(dP);
     f.slots = (ReduceSlot*)take(fusion_slots_bytes(kf->grid));
-    DF_CUDA(cudaMemsetAsync(f.slots, 0, fusion_slots_bytes(kf->grid), ctx->stream));
+    f.halo = resident ? (unsigned long long*)take(fusion_halo_bytes(P)) : nullptr;
     f.ctl = (FusionControl*)take(sizeof(FusionControl));
     kf->st = (FusionStateDev*)take(2 * sizeof(FusionStateDev));
     DF_CUDA(cudaMallocHost(&kf->h_ctl, sizeof(FusionControl)));
