@@ -750,7 +750,7 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
       ctl->stats.scale_step[k] = -1.0;
       ctl->stats.depth_step[k] = -1.0;
     }
-    if (threadIdx.x < 8) ctl->trace[threadIdx.x] = 0;
+    if (threadIdx.x < 16) ctl->trace[threadIdx.x] = 0;
     __syncthreads();
   }
 
@@ -795,7 +795,16 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
     const bool ls_mode = a.mode == DFUSE_MODE_LSSCALE;
     const bool depth_solvable = !ls_mode || inliers > 0;
     int cost_evals = 0, pcg_total = 0, gn_done = 0;
+    const bool otr = a.trace && leader;  // DFUSE_TRACE: cycles per GN phase, CTA 0
+    long long ot[5] = {0, 0, 0, 0, 0}, o_last = 0;
+#define DF_OTRACE(k)                \
+  if (otr) {                        \
+    const long long t_ = clock64(); \
+    ot[k] += t_ - o_last;           \
+    o_last = t_;                    \
+  }
     for (int it = 0; it < a.gn && status == 0; ++it) {
+      if (otr) o_last = clock64();
       if (!ls_mode && a.est_scale && inliers > 0) {  // fusion.hpp:411-425
         const double ln_s0 = log(scale);
         double ln_s = ln_s0;
@@ -815,6 +824,7 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
           }
         }
         cost_evals += 1;
+        DF_OTRACE(0);
         const double s_new = exp(ln_s);
         const double dlns = log(s_new) - log(scale);
         double step = 1.0, accepted = 0.0;
@@ -832,6 +842,7 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
           step *= 0.5;
         }
         if (leader && it < DFUSE_STATS_MAX_GN) ctl->stats.scale_step[it] = accepted;
+        DF_OTRACE(1);
       }
       if (depth_solvable) {  // fusion.hpp:426-441
         const double ln_s = sel.scale ? log(scale) : 0.0;
@@ -840,6 +851,7 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
         grid_allreduce(c, v);
         const double c0 = v[3];
         cost_evals += 1;
+        DF_OTRACE(2);
         int its = 0;
         if (v[0] != 0.0) {
           if (v[2] > 0.0) {
@@ -848,6 +860,7 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
             status = pcg_solve<PPT>(c, a, rg, v[0], v[1], &its);
           }
         }
+        DF_OTRACE(3);
         pcg_total += its;
         if (leader && it < DFUSE_STATS_MAX_GN) ctl->stats.pcg_iters[it] = its;
         if (status) break;
@@ -869,10 +882,14 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
           step *= 0.5;
         }
         if (leader && it < DFUSE_STATS_MAX_GN) ctl->stats.depth_step[it] = accepted;
+        DF_OTRACE(4);
       }
       iteration += 1;
       gn_done = it + 1;
     }
+#undef DF_OTRACE
+    if (otr)
+      for (int k = 0; k < 5; ++k) ctl->trace[8 + k] = ot[k];
     if (status == 0 && ls_mode) {  // fusion.hpp:445-452
       double v[1] = {0.0};
       const double* ld = a.ld[cur];
@@ -1095,7 +1112,7 @@ void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
     launch_fusion_t<0>(ctx, a, grid);
   DF_LAUNCHED(ctx);
   if (ctx->trace) {  // diagnostics only (DFUSE_TRACE=1): per-phase cycles of the resident PCG
-    long long tr[8];
+    long long tr[16];
     int its = 0;
     DF_CUDA(cudaMemcpyAsync(tr, a.ctl->trace, sizeof tr, cudaMemcpyDeviceToHost, ctx->stream));
     DF_CUDA(cudaMemcpyAsync(&its, &a.ctl->stats.pcg_total, sizeof its, cudaMemcpyDeviceToHost,
@@ -1103,8 +1120,10 @@ void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
     DF_CUDA(cudaStreamSynchronize(ctx->stream));
     fprintf(stderr,
             "dfuse trace (ppt %d, cycles, CTA 0): ring %lld own_p %lld spmv %lld ar1 %lld "
-            "sweepB %lld ar2 %lld\n",
-            a.ppt, tr[0], tr[1], tr[2], tr[3], tr[4], tr[5]);
+            "sweepB %lld ar2 %lld | scale %lld strial %lld assemble %lld pcg %lld dtrial %lld "
+            "(pcg its %d)\n",
+            a.ppt, tr[0], tr[1], tr[2], tr[3], tr[4], tr[5], tr[8], tr[9], tr[10], tr[11], tr[12],
+            its);
   }
 }
 

@@ -29,7 +29,7 @@ struct FusionControl {
   int pcg_last;
   double scale;
   double value[2];
-  long long trace[8];  // SM cycles per PCG phase, CTA 0 (DFUSE_TRACE=1)
+  long long trace[16];  // SM cycles per phase, CTA 0 (DFUSE_TRACE=1)
   dfuse_solver_stats stats;
 };
 
