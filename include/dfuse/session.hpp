@@ -1,0 +1,101 @@
+// dfuse/session.hpp -- the device-resident keyframe (replaces the hot part of
+// proj/include/dfuse/pipeline.hpp: make_keyframe 125-153 minus prediction
+// I/O, and process_frame 194-228 for tracked frames with retirement decided
+// by the caller).
+//
+//   dfuse::DeviceKeyframe kf(K, I0, predictions, cfg.texture_threshold);
+//   auto r = kf.process_frame(kf_pose, frame_pose, frame.intensity,
+//                             cfg.search, cfg.robust, cfg.mode);
+//   // r.observations, r.optimize_status (CgDivergence -> state unchanged,
+//   // exactly like run_sequence's skipped solve, pipeline.hpp:328-331)
+//   FusionState st = kf.fusion();  SemiDenseMap m = kf.semidense();
+#pragma once
+
+#include "dfuse/fusion.hpp"
+
+namespace dfuse {
+
+struct FrameOutcome {
+  int observations = 0;
+  int inlier_count = 0;
+  int stereo_frames = 0;
+  int optimize_status = 0;  // 0, or (int)Err + 1 of the error optimize threw
+  float stereo_ms = 0.f;
+  float optimise_ms = 0.f;
+  dfuse_solver_stats stats{};
+};
+
+class DeviceKeyframe {
+ public:
+  DeviceKeyframe(const CameraIntrinsics& K, const IntensityImage& I0, const PredictionSet& pred,
+                 double texture_threshold)
+      : K_(K) {
+    const dfuse_intrinsics k = K.c_abi();
+    const double* planes[6] = {pred.log_depth.data(), pred.log_depth_var.data(),
+                               pred.grad_x.data(),    pred.grad_x_var.data(),
+                               pred.grad_y.data(),    pred.grad_y_var.data()};
+    device::check(dfuse_kf_create(device::ctx(), &k, I0.raster().data(), planes,
+                                  texture_threshold, &kf_),
+                  "make_keyframe");
+  }
+  ~DeviceKeyframe() { dfuse_kf_destroy(kf_); }
+  DeviceKeyframe(const DeviceKeyframe&) = delete;
+  DeviceKeyframe& operator=(const DeviceKeyframe&) = delete;
+
+  FrameOutcome process_frame(const EpipolarGeometry& g, const IntensityImage& I1,
+                             const SearchConfig& search, const RobustConfig& robust,
+                             FusionMode mode) {
+    const dfuse_epigeom cg = g.c_abi();
+    const dfuse_search_cfg sc = search.c_abi();
+    const dfuse_robust_cfg rc = robust.c_abi();
+    dfuse_frame_result r;
+    device::check(dfuse_kf_process_frame(kf_, &cg, I1.raster().data(), &sc, &rc,
+                                         detail::mode_of(mode), &r),
+                  "process_frame");
+    return {r.observations, r.inlier_count, r.stereo_frames, r.optimize_status, r.stereo_ms,
+            r.optimise_ms, r.stats};
+  }
+
+  FrameOutcome process_frame(const Pose& keyframe_pose, const Pose& frame_pose,
+                             const IntensityImage& I1, const SearchConfig& search,
+                             const RobustConfig& robust, FusionMode mode) {
+    return process_frame(make_epipolar_geometry(keyframe_pose, frame_pose, K_), I1, search,
+                         robust, mode);
+  }
+
+  FusionState fusion() const {
+    FusionState st{Raster<double>(K_.width, K_.height, 0.0), 1.0, 0};
+    int32_t it = 0;
+    device::check(dfuse_kf_download(kf_, st.log_depth.data(), &st.scale, &it, nullptr, nullptr,
+                                    nullptr, nullptr, nullptr),
+                  "download");
+    st.iteration = it;
+    return st;
+  }
+
+  SemiDenseMap semidense() const {
+    SemiDenseMap m = SemiDenseMap::empty(K_.width, K_.height);
+    int32_t count = 0;
+    device::check(dfuse_kf_download(kf_, nullptr, nullptr, nullptr, m.depth.data(),
+                                    m.variance.data(), m.valid.data(), &count, nullptr),
+                  "download");
+    m.inlier_count = count;
+    return m;
+  }
+
+  Mask texture() const {
+    Mask m(K_.width, K_.height, 0);
+    device::check(dfuse_kf_download(kf_, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                    nullptr, m.data()),
+                  "download");
+    return m;
+  }
+
+  void reset() { device::check(dfuse_kf_reset(kf_), "reset"); }
+
+ private:
+  CameraIntrinsics K_;
+  dfuse_keyframe* kf_ = nullptr;
+};
+
+}  // namespace dfuse

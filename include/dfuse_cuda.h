@@ -185,6 +185,12 @@ int dfuse_search_depth(dfuse_ctx* ctx, const dfuse_epigeom* g, const float* I0, 
                        const dfuse_search_cfg* cfg, int32_t* status, dfuse_obs* obs,
                        int32_t* best, int32_t* n_steps);
 
+/* photometric_error_5pt(g, I0, I1, x, d, e), semidense.hpp:227-243: the five
+ * stencil residuals at one depth hypothesis; *status = DFUSE_EPI_* */
+int dfuse_photometric_error_5pt(dfuse_ctx* ctx, const dfuse_epigeom* g, const float* I0,
+                                const float* I1, double x, double y, double d, double e[5],
+                                int32_t* status);
+
 /* update_semidense(map, observations), semidense.hpp:393-417. The map is
  * updated in place (depth, variance, valid, inlier_count). Observations are
  * applied in list order (duplicates of one pixel fuse sequentially). */

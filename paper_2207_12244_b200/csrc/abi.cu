@@ -367,6 +367,27 @@ int dfuse_search_depth(dfuse_ctx* ctx, const dfuse_epigeom* g, const float* I0, 
   });
 }
 
+int dfuse_photometric_error_5pt(dfuse_ctx* ctx, const dfuse_epigeom* g, const float* I0,
+                                const float* I1, double x, double y, double d, double e[5],
+                                int32_t* status) {
+  return guarded(ctx, [&] {
+    check_geom(g);
+    require(I0 && I1 && e && status, DFUSE_E_INVALID_ARGUMENT, "null pointer");
+    const long P = (long)g->K.width * g->K.height;
+    float* d0 = (float*)scratch(ctx, S_IMG0, sizeof(float) * P);
+    float* d1 = (float*)scratch(ctx, S_IMG1, sizeof(float) * P);
+    double* out = (double*)scratch(ctx, S_TMP3, 8 * sizeof(double));
+    h2d(ctx, d0, I0, sizeof(float) * P);
+    h2d(ctx, d1, I1, sizeof(float) * P);
+    launch_photometric(ctx, *g, d0, d1, x, y, d, out);
+    double h[6];
+    d2h(ctx, h, out, sizeof h);
+    sync(ctx);
+    for (int j = 0; j < 5; ++j) e[j] = h[j];
+    *status = (int32_t)h[5];
+  });
+}
+
 int dfuse_update_semidense(dfuse_ctx* ctx, int w, int h, double* depth, double* variance,
                            uint8_t* valid, int32_t* inlier_count, int n_obs,
                            const dfuse_obs* obs) {

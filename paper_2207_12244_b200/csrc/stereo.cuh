@@ -38,6 +38,8 @@ struct StereoArgs {
   uint8_t* obs_flag;
 };
 
+void launch_photometric(dfuse_ctx* ctx, const dfuse_epigeom& g, const float* I0, const float* I1,
+                        double x, double y, double d, double* out);
 void launch_texture_mask(dfuse_ctx* ctx, const float* img, int w, int h, double threshold,
                          uint8_t* mask);
 void launch_mask_list(dfuse_ctx* ctx, const uint8_t* mask, long P, int* list, int* count);
