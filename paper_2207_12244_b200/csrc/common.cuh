@@ -122,6 +122,13 @@ __device__ __forceinline__ double glibc_hypot(double x, double y) {
   return glibc_hypot_kernel(ax, ay);
 }
 
+// device wall clock in ns (diagnostics: DFUSE_TRACE)
+__device__ __forceinline__ long long df_now() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // deterministic warp sum: fixed butterfly order, identical on every lane
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

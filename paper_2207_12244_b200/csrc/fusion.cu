@@ -110,15 +110,32 @@ __device__ __forceinline__ double ll_value(unsigned long long w0, unsigned long 
   return __longlong_as_double(
       (long long)(((w1 & 0xffffffffULL) << 32) | (w0 & 0xffffffffULL)));
 }
+// the two words of one double travel in one 16-byte access (each 8-byte
+// element is single-copy atomic, which is all the LL protocol needs)
+__device__ __forceinline__ void ld_relaxed_v2(const unsigned long long* p, unsigned long long& a,
+                                              unsigned long long& b) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+               : "=l"(a), "=l"(b)
+               : "l"(p)
+               : "memory");
+}
+__device__ __forceinline__ void st_relaxed_v2(unsigned long long* p, unsigned long long a,
+                                              unsigned long long b) {
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b)
+               : "memory");
+}
 __device__ __forceinline__ void ll_store(unsigned long long* p, double v, unsigned flag) {
+#if DFUSE_LL_V2_HALO
+  st_relaxed_v2(p, ll_word(v, 0, flag), ll_word(v, 1, flag));
+#else
   st_relaxed_u64(p, ll_word(v, 0, flag));
   st_relaxed_u64(p + 1, ll_word(v, 1, flag));
+#endif
 }
 __device__ __forceinline__ double ll_wait(const unsigned long long* p, unsigned flag) {
   unsigned long long w0, w1;
   do {
-    w0 = ld_relaxed_u64(p);
-    w1 = ld_relaxed_u64(p + 1);
+    ld_relaxed_v2(p, w0, w1);
   } while ((unsigned)(w0 >> 32) != flag || (unsigned)(w1 >> 32) != flag);
   return ll_value(w0, w1);
 }
@@ -157,20 +174,33 @@ __device__ void grid_allreduce(GridCtx& c, double (&v)[NV]) {
     double acc[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) acc[k] = 0.0;
-    if (VARIANT == 10) {
+    if (VARIANT == 13) {
+      // microbenchmark only: the CTA-local part of the all-reduce (no exchange)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) acc[k] = lane == 0 ? t[k] : 0.0;
+    } else if (VARIANT == 10 || VARIANT == 12) {
       constexpr int NW = 2 * NV;
       const unsigned flag = c.phase + 1;
       // parity buffers: a CTA may publish phase k+1 while a slow CTA still
       // polls its phase-k words
       unsigned long long* ll =
           reinterpret_cast<unsigned long long*>(c.slots) + (size_t)(c.phase & 1) * c.G * 8;
-      if (lane < NW) {
+      if (lane < (VARIANT == 12 ? NW : NV)) {
         double tk = t[0];
+        const int kk = VARIANT == 12 ? (lane >> 1) : lane;
 #pragma unroll
         for (int k = 1; k < NV; ++k)
-          if ((lane >> 1) == k) tk = t[k];
-        st_relaxed_u64(ll + (size_t)blockIdx.x * 8 + lane, ll_word(tk, lane & 1, flag));
-        __threadfence();  // push the words (and, cumulatively, the CTA's writes) to L2
+          if (kk == k) tk = t[k];
+        if (VARIANT == 12) {
+          // atomic exchange: performed at L2, no write-back buffering
+          atomicExch(ll + (size_t)blockIdx.x * 8 + lane, ll_word(tk, lane & 1, flag));
+          if (FENCE) __threadfence();
+        } else {
+          // lane k publishes value k as one 16-byte {low, high} LL pair
+          st_relaxed_v2(ll + (size_t)blockIdx.x * 8 + 2 * lane, ll_word(tk, 0, flag),
+                        ll_word(tk, 1, flag));
+          __threadfence();  // push the words (and, cumulatively, the CTA's writes) to L2
+        }
       }
       // every round loads all of this lane's slots at once and sums them
       // speculatively (fixed order); the round whose flags all match wins
@@ -185,8 +215,8 @@ __device__ void grid_allreduce(GridCtx& c, double (&v)[NV]) {
           if (b < c.G) {
 #pragma unroll
             for (int k = 0; k < NV; ++k) {
-              const unsigned long long w0 = ld_relaxed_u64(ll + (size_t)b * 8 + 2 * k);
-              const unsigned long long w1 = ld_relaxed_u64(ll + (size_t)b * 8 + 2 * k + 1);
+              unsigned long long w0, w1;
+              ld_relaxed_v2(ll + (size_t)b * 8 + 2 * k, w0, w1);
               ok &= (unsigned)(w0 >> 32) == flag && (unsigned)(w1 >> 32) == flag;
               accr[k] += ll_value(w0, w1);
             }
@@ -267,7 +297,7 @@ __device__ __forceinline__ double pixel_cost(const FusionArgs& a, const Sel& sel
   double c = 0.0;
   if (sel.net) c += huber_c(li - a.pred[0][i], a.dnet) / a.pred[1][i];
   if (a.svalid[i])
-    c += huber_c(li - ln_s - log(a.sd[i]), a.dsemi) / semi_logvar(a.sv[i], a.sd[i]);
+    c += huber_c(li - ln_s - a.lnsd[i], a.dsemi) / a.semR[i];
   if (sel.grad && x + 1 < a.W) c += huber_c(L(i + 1) - li - a.pred[2][i], a.dgrad) / a.pred[3][i];
   if (sel.grad && y + 1 < a.H)
     c += huber_c(L(i + a.W) - li - a.pred[4][i], a.dgrad) / a.pred[5][i];
@@ -287,21 +317,41 @@ __device__ __forceinline__ Range my_range(const FusionArgs& a) {
 }
 
 // ---------------------------------------------------------------------------
-// sweeps
+// sweeps (every sweep walks the CTA's range with the same thread->pixel map,
+// so per-pixel values a thread writes are read back by that thread)
+
+// per-call constants of the semi term: ln d_semi and R = semi_log_variance
+// (fusion.hpp:95-100,195-196), computed once instead of in every sweep
+__device__ void sweep_semi_prologue(const FusionArgs& a, const Range& rg) {
+  for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT)
+    if (a.svalid[i]) {
+      a.lnsd[i] = log(a.sd[i]);
+      a.semR[i] = semi_logvar(a.sv[i], a.sd[i]);
+    }
+}
+
 // scale IRLS round (fusion.hpp:379-388) [+ total_cost at ln_s_cost]
+// stage (optional, shared memory): offset and R of the CTA's pixels for the
+// later rounds (R = -1 marks a pixel without a semi-dense value)
 __device__ void sweep_scale(const FusionArgs& a, const Sel& sel, const Range& rg,
                             const double* ld, double ln_s, bool with_cost, double ln_s_cost,
-                            double (&v)[4]) {
+                            double (&v)[4], double* stage = nullptr, int stage_n = 0) {
   double num = 0.0, den = 0.0, cost = 0.0;
   PlainLd L{ld};
   for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) {
     const double li = ld[i];
     if (a.svalid[i]) {
-      const double offset = li - log(a.sd[i]);
-      const double R = semi_logvar(a.sv[i], a.sd[i]);
+      const double offset = li - a.lnsd[i];
+      const double R = a.semR[i];
       const double wi = huber_w(offset - ln_s, a.dsemi) / R;
       num += wi * offset;
       den += wi;
+      if (stage) {
+        stage[i - rg.beg] = offset;
+        stage[stage_n + i - rg.beg] = R;
+      }
+    } else if (stage) {
+      stage[stage_n + i - rg.beg] = -1.0;
     }
     if (with_cost) {
       const int y = i / a.W, x = i - y * a.W;
@@ -312,6 +362,24 @@ __device__ void sweep_scale(const FusionArgs& a, const Sel& sel, const Range& rg
   v[1] = den;
   v[2] = cost;
   v[3] = 0.0;
+}
+
+// scale IRLS rounds 1 and 2 from the values staged by round 0 (same
+// arithmetic, same per-thread order as sweep_scale)
+__device__ void sweep_scale_staged(const FusionArgs& a, const Range& rg, const double* stage,
+                                   int stage_n, double ln_s, double (&v)[2]) {
+  double num = 0.0, den = 0.0;
+  for (int k = threadIdx.x; k < rg.end - rg.beg; k += FT) {
+    const double R = stage[stage_n + k];
+    if (R != -1.0) {
+      const double offset = stage[k];
+      const double wi = huber_w(offset - ln_s, a.dsemi) / R;
+      num += wi * offset;
+      den += wi;
+    }
+  }
+  v[0] = num;
+  v[1] = den;
 }
 
 template <class LD>
@@ -362,8 +430,8 @@ __device__ void sweep_assemble(const FusionArgs& a, const Sel& sel, const Range&
       b -= wi * r;
     }
     if (a.svalid[i]) {
-      const double r = li - ln_s - log(a.sd[i]);
-      const double R = semi_logvar(a.sv[i], a.sd[i]);
+      const double r = li - ln_s - a.lnsd[i];
+      const double R = a.semR[i];
       const double wi = huber_w(r, a.dsemi) / R;
       diag += wi;
       b -= wi * r;
@@ -584,10 +652,10 @@ __device__ int pcg_resident_v1(GridCtx& c, const FusionArgs& a, double bnorm2, d
   *its = 0;
   // DFUSE_TRACE: CTA 0 / thread 0 accumulates SM cycles per phase
   const bool tracer = a.trace && blockIdx.x == 0 && threadIdx.x == 0;
-  long long tr[6] = {0, 0, 0, 0, 0, 0}, t_last = tracer ? clock64() : 0;
+  long long tr[6] = {0, 0, 0, 0, 0, 0}, t_last = tracer ? df_now() : 0;
 #define DF_TRACE(k)                 \
   if (tracer) {                     \
-    const long long t_ = clock64(); \
+    const long long t_ = df_now(); \
     tr[k] += t_ - t_last;           \
     t_last = t_;                    \
   }
@@ -753,6 +821,7 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
     if (threadIdx.x < 16) ctl->trace[threadIdx.x] = 0;
     __syncthreads();
   }
+  if (a.op != OP_PCG) sweep_semi_prologue(a, rg);
 
   if (a.op == OP_COST) {
     double v[1] = {sweep_cost(a, sel, rg, PlainLd{a.ld[0]}, sel.scale ? log(a.scale0) : 0.0,
@@ -799,26 +868,37 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
     long long ot[5] = {0, 0, 0, 0, 0}, o_last = 0;
 #define DF_OTRACE(k)                \
   if (otr) {                        \
-    const long long t_ = clock64(); \
+    const long long t_ = df_now(); \
     ot[k] += t_ - o_last;           \
     o_last = t_;                    \
   }
     for (int it = 0; it < a.gn && status == 0; ++it) {
-      if (otr) o_last = clock64();
+      if (otr) o_last = df_now();
       if (!ls_mode && a.est_scale && inliers > 0) {  // fusion.hpp:411-425
         const double ln_s0 = log(scale);
         double ln_s = ln_s0;
         double c0 = 0.0;
+        extern __shared__ double dsm_stage[];
+        double* stage = a.stage_n > 0 ? dsm_stage : nullptr;
         for (int round = 0; round < 3; ++round) {
-          double v[4];
-          sweep_scale(a, sel, rg, a.ld[cur], ln_s, round == 0, sel.scale ? ln_s0 : 0.0, v);
           if (round == 0) {
+            double v[4];
+            sweep_scale(a, sel, rg, a.ld[cur], ln_s, true, sel.scale ? ln_s0 : 0.0, v, stage,
+                        a.stage_n);
             double w[3] = {v[0], v[1], v[2]};
             grid_allreduce(c, w);
             c0 = w[2];
             ln_s = w[0] / w[1];
           } else {
-            double w[2] = {v[0], v[1]};
+            double w[2];
+            if (stage) {
+              sweep_scale_staged(a, rg, stage, a.stage_n, ln_s, w);
+            } else {
+              double v[4];
+              sweep_scale(a, sel, rg, a.ld[cur], ln_s, false, 0.0, v);
+              w[0] = v[0];
+              w[1] = v[1];
+            }
             grid_allreduce(c, w);
             ln_s = w[0] / w[1];
           }
@@ -933,6 +1013,7 @@ __global__ void __launch_bounds__(FT, 1) k_gradient(FusionArgs a, double* g) {
   const int W = a.W, H = a.H;
   const double* ld = a.ld[0];
   PlainLd L{ld};
+  sweep_semi_prologue(a, rg);
   double cost = 0.0, gs = 0.0;
   for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) {
     const int y = i / W, x = i - y * W;
@@ -953,8 +1034,8 @@ __global__ void __launch_bounds__(FT, 1) k_gradient(FusionArgs a, double* g) {
       gi += 2.0 * huber_w(r, a.dnet) * r / a.pred[1][i];
     }
     if (a.svalid[i]) {
-      const double R = semi_logvar(a.sv[i], a.sd[i]);
-      const double r = li - ln_s - log(a.sd[i]);
+      const double R = a.semR[i];
+      const double r = li - ln_s - a.lnsd[i];
       const double d = 2.0 * huber_w(r, a.dsemi) * r / R;
       gi += d;
       if (sel.scale) gs -= d;
@@ -1004,7 +1085,7 @@ __global__ void __launch_bounds__(FT, 1) k_sync_bench(ReduceSlot* slots, unsigne
   double acc = 0.0;
   for (int i = 0; i < n; ++i) {
     double v[2] = {1.0, (double)threadIdx.x};
-    grid_allreduce<2, VARIANT != 10, VARIANT>(c, v);
+    grid_allreduce<2, VARIANT < 10, VARIANT>(c, v);
     acc += v[0];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *out = acc;
@@ -1096,6 +1177,12 @@ static void launch_fusion_t(dfuse_ctx* ctx, FusionArgs& a, int grid) {
 void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
   plan_tiles(a, grid);
   if (ctx->force_streaming) a.ppt = 0;
+  {  // scale-round staging lives in the resident PCG's shared memory
+    const long range = ((long)a.W * a.H + grid - 1) / grid;
+    a.stage_n = (a.ppt > 0 && (size_t)(16 * range) <= pcg_tile_smem(a.tw_max, a.th_max))
+                    ? (int)range
+                    : 0;
+  }
   a.base_tag = next_tag();
   // LL flags restart at 1 every launch: clear the slots and the halo words
   DF_CUDA(cudaMemsetAsync(a.slots, 0, fusion_slots_bytes(grid), ctx->stream));
@@ -1119,7 +1206,7 @@ void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
                             ctx->stream));
     DF_CUDA(cudaStreamSynchronize(ctx->stream));
     fprintf(stderr,
-            "dfuse trace (ppt %d, cycles, CTA 0): ring %lld own_p %lld spmv %lld ar1 %lld "
+            "dfuse trace (ppt %d, ns, CTA 0): ring %lld own_p %lld spmv %lld ar1 %lld "
             "sweepB %lld ar2 %lld | scale %lld strial %lld assemble %lld pcg %lld dtrial %lld "
             "(pcg its %d)\n",
             a.ppt, tr[0], tr[1], tr[2], tr[3], tr[4], tr[5], tr[8], tr[9], tr[10], tr[11], tr[12],
@@ -1144,9 +1231,11 @@ float sync_bench(dfuse_ctx* ctx, int n, int variant, int grid) {
   DF_CUDA(cudaMemsetAsync(slots, 0, bytes, ctx->stream));
   unsigned long long tag = next_tag();
   void* args[] = {&slots, &tag, &n, &out};
-  const void* fn = variant == 1   ? (const void*)k_sync_bench<1>
-                   : variant == 2 ? (const void*)k_sync_bench<2>
-                                  : (const void*)k_sync_bench<10>;
+  const void* fn = variant == 1    ? (const void*)k_sync_bench<1>
+                   : variant == 2  ? (const void*)k_sync_bench<2>
+                   : variant == 12 ? (const void*)k_sync_bench<12>
+                   : variant == 13 ? (const void*)k_sync_bench<13>
+                                   : (const void*)k_sync_bench<10>;
   DF_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
   DF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(FT), args, 0, ctx->stream));
   DF_LAUNCHED(ctx);

@@ -39,6 +39,8 @@ struct FusionArgs {
   const double* sd;
   const double* sv;
   const uint8_t* svalid;
+  double* lnsd;  // log(semi depth), filled by the kernel prologue (valid pixels)
+  double* semR;  // semi_log_variance(variance, depth), same
   int inlier_count;
   const int* inlier_dev;  // if set, overrides inlier_count (device-resident session)
   double dsemi, dnet, dgrad, cg_tol;
@@ -61,6 +63,7 @@ struct FusionArgs {
   unsigned long long* halo;     // resident PCG LL halo words [3][P][2], or null
   int tiles_x, tiles_y, tw_max, th_max, ppt;  // resident-PCG tiling (set by launch_fusion)
   int trace;  // record per-phase cycle counts of the resident PCG in ctl->trace
+  int stage_n;  // > 0: scale rounds 1-2 read round 0's values from shared memory
   FusionControl* ctl;
 };
 

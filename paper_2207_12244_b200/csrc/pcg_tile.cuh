@@ -89,10 +89,10 @@ __device__ int pcg_resident(GridCtx& c, const FusionArgs& a, double bnorm2, doub
   *its = 0;
   // DFUSE_TRACE: CTA 0 / thread 0 accumulates SM cycles per phase
   const bool tracer = a.trace && blockIdx.x == 0 && threadIdx.x == 0;
-  long long tr[6] = {0, 0, 0, 0, 0, 0}, t_last = tracer ? clock64() : 0;
+  long long tr[6] = {0, 0, 0, 0, 0, 0}, t_last = tracer ? df_now() : 0;
 #define DF_TRACE(k)                 \
   if (tracer) {                     \
-    const long long t_ = clock64(); \
+    const long long t_ = df_now(); \
     tr[k] += t_ - t_last;           \
     t_last = t_;                    \
   }
@@ -118,13 +118,18 @@ __device__ int pcg_resident(GridCtx& c, const FusionArgs& a, double bnorm2, doub
         const unsigned long long* zw = z_ll + 2 * j;
         const unsigned long long* pwd = p_ll[(it + 1) & 1] + 2 * j;
         unsigned long long z0, z1, p0 = (unsigned long long)fp << 32, p1 = p0;
-        for (;;) {  // all four words in flight per round
+        for (;;) {  // all words in flight per round
+#if DFUSE_LL_V2_HALO
+          ld_relaxed_v2(zw, z0, z1);
+          if (!first) ld_relaxed_v2(pwd, p0, p1);
+#else
           z0 = ld_relaxed_u64(zw);
           z1 = ld_relaxed_u64(zw + 1);
           if (!first) {
             p0 = ld_relaxed_u64(pwd);
             p1 = ld_relaxed_u64(pwd + 1);
           }
+#endif
           if ((unsigned)(z0 >> 32) == fz && (unsigned)(z1 >> 32) == fz &&
               (unsigned)(p0 >> 32) == fp && (unsigned)(p1 >> 32) == fp)
             break;
