@@ -40,6 +40,9 @@
 #include <math.h>
 #include <stdio.h>
 
+#include <algorithm>
+#include <vector>
+
 #include "common.cuh"
 #include "fusion.cuh"
 
@@ -178,7 +181,7 @@ __device__ void grid_allreduce(GridCtx& c, double (&v)[NV]) {
       // microbenchmark only: the CTA-local part of the all-reduce (no exchange)
 #pragma unroll
       for (int k = 0; k < NV; ++k) acc[k] = lane == 0 ? t[k] : 0.0;
-    } else if (VARIANT == 10 || VARIANT == 12) {
+    } else if (VARIANT == 10 || VARIANT == 12 || VARIANT == 14 || VARIANT == 15) {
       constexpr int NW = 2 * NV;
       const unsigned flag = c.phase + 1;
       // parity buffers: a CTA may publish phase k+1 while a slow CTA still
@@ -195,11 +198,23 @@ __device__ void grid_allreduce(GridCtx& c, double (&v)[NV]) {
           // atomic exchange: performed at L2, no write-back buffering
           atomicExch(ll + (size_t)blockIdx.x * 8 + lane, ll_word(tk, lane & 1, flag));
           if (FENCE) __threadfence();
+        } else if (VARIANT == 14 || VARIANT == 15) {
+          // microbenchmark: no fence; L2-only (14) or volatile (15) 16-byte store
+          unsigned long long* dst = ll + (size_t)blockIdx.x * 8 + 2 * lane;
+          const unsigned long long w0 = ll_word(tk, 0, flag), w1 = ll_word(tk, 1, flag);
+          if (VARIANT == 14)
+            asm volatile("st.global.cg.v2.u64 [%0], {%1, %2};" ::"l"(dst), "l"(w0), "l"(w1)
+                         : "memory");
+          else
+            asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(dst), "l"(w0),
+                         "l"(w1)
+                         : "memory");
         } else {
-          // lane k publishes value k as one 16-byte {low, high} LL pair
+          // lane k publishes value k as one 16-byte {low, high} LL pair; with
+          // FENCE the fence also publishes the CTA's earlier global writes
           st_relaxed_v2(ll + (size_t)blockIdx.x * 8 + 2 * lane, ll_word(tk, 0, flag),
                         ll_word(tk, 1, flag));
-          __threadfence();  // push the words (and, cumulatively, the CTA's writes) to L2
+          if (FENCE) __threadfence();
         }
       }
       // every round loads all of this lane's slots at once and sums them
@@ -274,6 +289,89 @@ __device__ void grid_allreduce(GridCtx& c, double (&v)[NV]) {
 __device__ __forceinline__ void grid_sync(GridCtx& c) {
   double none[1] = {0.0};
   grid_allreduce(c, none);
+}
+
+// Split-phase LL all-reduce (no fence): publish() reduces the CTA's partials
+// and posts them; the CTA may then do independent work (the resident PCG
+// runs its next SpMV there) before wait() collects the grid sum. No other
+// all-reduce may run in between.
+__device__ __forceinline__ double* split_smem() {
+  __shared__ double s[FW * 4 + 4];
+  return s;
+}
+
+template <int NV>
+__device__ void grid_allreduce_publish(GridCtx& c, double (&v)[NV]) {
+  double* red = split_smem();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) red[wid * 4 + k] = v[k];
+  __syncthreads();
+  if (wid == 0) {
+    double t[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) t[k] = warp_sum(lane < FW ? red[lane * 4 + k] : 0.0);
+    const unsigned flag = c.phase + 1;
+    unsigned long long* ll =
+        reinterpret_cast<unsigned long long*>(c.slots) + (size_t)(c.phase & 1) * c.G * 8;
+    if (lane < NV) {
+      double tk = t[0];
+#pragma unroll
+      for (int k = 1; k < NV; ++k)
+        if (lane == k) tk = t[k];
+      st_relaxed_v2(ll + (size_t)blockIdx.x * 8 + 2 * lane, ll_word(tk, 0, flag),
+                    ll_word(tk, 1, flag));
+    }
+  }
+}
+
+template <int NV>
+__device__ void grid_allreduce_wait(GridCtx& c, double (&v)[NV]) {
+  double* bc = split_smem() + FW * 4;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (wid == 0) {
+    const unsigned flag = c.phase + 1;
+    const unsigned long long* ll =
+        reinterpret_cast<unsigned long long*>(c.slots) + (size_t)(c.phase & 1) * c.G * 8;
+    double acc[NV];
+    for (;;) {
+      bool ok = true;
+      double accr[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) accr[k] = 0.0;
+#pragma unroll
+      for (int m = 0; m < kMaxPollSlots; ++m) {
+        const unsigned b = lane + 32 * m;
+        if (b < c.G) {
+#pragma unroll
+          for (int k = 0; k < NV; ++k) {
+            unsigned long long w0, w1;
+            ld_relaxed_v2(ll + (size_t)b * 8 + 2 * k, w0, w1);
+            ok &= (unsigned)(w0 >> 32) == flag && (unsigned)(w1 >> 32) == flag;
+            accr[k] += ll_value(w0, w1);
+          }
+        }
+      }
+      if (__all_sync(0xffffffffu, ok)) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) acc[k] = accr[k];
+        break;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] = warp_sum(acc[k]);
+    if (lane == 0)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) bc[k] = acc[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = bc[k];
+  c.phase += 1;
+  c.syncs += 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -1189,6 +1287,11 @@ void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
   if (a.ppt > 0)
     DF_CUDA(cudaMemsetAsync(a.halo, 0, fusion_halo_bytes((long)a.W * a.H), ctx->stream));
   a.trace = ctx->trace;
+  a.dbg = nullptr;
+  if (ctx->trace >= 2) {
+    a.dbg = (long long*)scratch(ctx, S_TMP4, sizeof(long long) * 8 * grid);
+    DF_CUDA(cudaMemsetAsync(a.dbg, 0, sizeof(long long) * 8 * grid, ctx->stream));
+  }
   if (a.ppt == 4)
     launch_fusion_t<4>(ctx, a, grid);
   else if (a.ppt == 5)
@@ -1206,11 +1309,22 @@ void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
                             ctx->stream));
     DF_CUDA(cudaStreamSynchronize(ctx->stream));
     fprintf(stderr,
-            "dfuse trace (ppt %d, ns, CTA 0): ring %lld own_p %lld spmv %lld ar1 %lld "
-            "sweepB %lld ar2 %lld | scale %lld strial %lld assemble %lld pcg %lld dtrial %lld "
+            "dfuse trace (ppt %d, ns, CTA 0): ring %lld spmv %lld wait_rz %lld pq_upd %lld "
+            "ar_pq %lld sweepB_pub %lld | scale %lld strial %lld assemble %lld pcg %lld dtrial %lld "
             "(pcg its %d)\n",
             a.ppt, tr[0], tr[1], tr[2], tr[3], tr[4], tr[5], tr[8], tr[9], tr[10], tr[11], tr[12],
             its);
+    if (a.dbg) {  // per-CTA spread of each phase
+      std::vector<long long> h((size_t)8 * grid);
+      DF_CUDA(cudaMemcpy(h.data(), a.dbg, sizeof(long long) * 8 * grid, cudaMemcpyDeviceToHost));
+      for (int k = 0; k < 6; ++k) {
+        std::vector<long long> col(grid);
+        for (int b = 0; b < grid; ++b) col[b] = h[(size_t)b * 8 + k];
+        std::sort(col.begin(), col.end());
+        fprintf(stderr, "  phase %d across CTAs: min %lld median %lld max %lld\n", k, col[0],
+                col[grid / 2], col[grid - 1]);
+      }
+    }
   }
 }
 
@@ -1235,6 +1349,8 @@ float sync_bench(dfuse_ctx* ctx, int n, int variant, int grid) {
                    : variant == 2  ? (const void*)k_sync_bench<2>
                    : variant == 12 ? (const void*)k_sync_bench<12>
                    : variant == 13 ? (const void*)k_sync_bench<13>
+                   : variant == 14 ? (const void*)k_sync_bench<14>
+                   : variant == 15 ? (const void*)k_sync_bench<15>
                                    : (const void*)k_sync_bench<10>;
   DF_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
   DF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(FT), args, 0, ctx->stream));

@@ -64,6 +64,7 @@ struct FusionArgs {
   int tiles_x, tiles_y, tw_max, th_max, ppt;  // resident-PCG tiling (set by launch_fusion)
   int trace;  // record per-phase cycle counts of the resident PCG in ctl->trace
   int stage_n;  // > 0: scale rounds 1-2 read round 0's values from shared memory
+  long long* dbg;  // DFUSE_TRACE=2: per-CTA phase times [grid][8]
   FusionControl* ctl;
 };
 
