@@ -48,9 +48,11 @@
 
 namespace dfuse_cuda {
 
-constexpr int FT = 512;  // threads per CTA
+constexpr int FT = 512;  // threads per CTA (one CTA per SM)
 constexpr int FW = FT / 32;
-constexpr int kMaxPollSlots = 8;  // each lane polls <= 8 CTA slots: grids up to 256
+// each lane polls <= 5 CTA slots (grids up to 160 CTAs: B200 has 148 SMs);
+// the unrolled poll keeps all of them in flight, so this bounds registers
+constexpr int kMaxPollSlots = 5;
 
 struct Sel {
   bool net, grad, scale;
@@ -1311,8 +1313,9 @@ void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
     fprintf(stderr,
             "dfuse trace (ppt %d, ns, CTA 0): ring %lld spmv %lld wait_rz %lld pq_upd %lld "
             "ar_pq %lld sweepB_pub %lld | scale %lld strial %lld assemble %lld pcg %lld dtrial %lld "
-            "(pcg its %d)\n",
+            "(pcg its %d) sm_clock %.0f MHz\n",
             a.ppt, tr[0], tr[1], tr[2], tr[3], tr[4], tr[5], tr[8], tr[9], tr[10], tr[11], tr[12],
+            tr[6] > 0 ? 1e3 * (double)tr[7] / (double)tr[6] : 0.0,
             its);
     if (a.dbg) {  // per-CTA spread of each phase
       std::vector<long long> h((size_t)8 * grid);

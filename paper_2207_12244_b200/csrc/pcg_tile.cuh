@@ -50,13 +50,15 @@ __device__ int pcg_resident(GridCtx& c, const FusionArgs& a, double bnorm2, doub
   for (int t = threadIdx.x; t < (tg.th + 2) * pw; t += FT) s_z[t] = 0.0;
   __syncthreads();
 
-  double xr[PPT], rr_[PPT], zr[PPT], pr[PPT], qr[PPT];
+  double* s_x = s_z + (a.th_max + 2) * (a.tw_max + 2);  // x lives in shared memory
+  double rr_[PPT], zr[PPT], pr[PPT], qr[PPT];
   int so_[PPT];  // offset in s_z
   int gi_[PPT];  // global pixel index (-1: no pixel); bit 30 set: tile boundary
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
     const int k = threadIdx.x + FT * j;
-    xr[j] = rr_[j] = zr[j] = pr[j] = qr[j] = 0.0;
+    rr_[j] = zr[j] = pr[j] = qr[j] = 0.0;
+    if (k < T) s_x[k] = 0.0;
     gi_[j] = -1;
     so_[j] = 0;
     if (k < T) {
@@ -94,6 +96,7 @@ __device__ int pcg_resident(GridCtx& c, const FusionArgs& a, double bnorm2, doub
   // every CTA -> a.dbg[cta][phase] when DFUSE_TRACE=2)
   const bool tracer = a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || a.dbg);
   long long tr[6] = {0, 0, 0, 0, 0, 0}, t_last = tracer ? df_now() : 0;
+  const long long t_start = t_last, c_start = tracer ? clock64() : 0;
 #define DF_TRACE(k)               \
   if (tracer) {                   \
     const long long t_ = df_now(); \
@@ -186,7 +189,7 @@ __device__ int pcg_resident(GridCtx& c, const FusionArgs& a, double bnorm2, doub
     for (int j = 0; j < PPT; ++j) {
       if (gi_[j] >= 0) {
         const int k = threadIdx.x + FT * j;
-        xr[j] = xr[j] + alpha * pr[j];
+        s_x[k] = s_x[k] + alpha * pr[j];
         const double r = rr_[j] - alpha * qr[j];
         rr_[j] = r;
         rr += r * r;
@@ -206,8 +209,11 @@ __device__ int pcg_resident(GridCtx& c, const FusionArgs& a, double bnorm2, doub
     DF_TRACE(5);
   }
 #undef DF_TRACE
-  if (tracer && blockIdx.x == 0)
+  if (tracer && blockIdx.x == 0) {
     for (int k = 0; k < 6; ++k) a.ctl->trace[k] += tr[k];
+    a.ctl->trace[6] += df_now() - t_start;  // ns
+    a.ctl->trace[7] += clock64() - c_start;  // SM cycles -> effective clock
+  }
   if (tracer && a.dbg)
     for (int k = 0; k < 6; ++k) a.dbg[blockIdx.x * 8 + k] += tr[k];
   if (pending) {  // broke out before collecting: keep the phase counter in step
@@ -217,12 +223,12 @@ __device__ int pcg_resident(GridCtx& c, const FusionArgs& a, double bnorm2, doub
   // delta to the raster for the line search (x == 0 if no iteration ran)
 #pragma unroll
   for (int j = 0; j < PPT; ++j)
-    if (gi_[j] >= 0) a.x[gi_[j] & ~(1 << 30)] = xr[j];
+    if (gi_[j] >= 0) a.x[gi_[j] & ~(1 << 30)] = s_x[threadIdx.x + FT * j];
   grid_sync(c);  // fenced: the trial sweeps read x at the neighbours
   return status;
 }
 
 // shared memory of pcg_resident for a tw_max x th_max tile
 inline size_t pcg_tile_smem(int tw_max, int th_max) {
-  return sizeof(double) * (6 * (size_t)tw_max * th_max + (size_t)(th_max + 2) * (tw_max + 2));
+  return sizeof(double) * (7 * (size_t)tw_max * th_max + (size_t)(th_max + 2) * (tw_max + 2));
 }
