@@ -67,6 +67,16 @@ def dist_env():
     return ws, rank, local
 
 
+def ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of `kernel`
+    from the committed ncu capture (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return int(json.load(f)[kernel]["dram_bytes_per_launch"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -379,7 +389,8 @@ def main():
         "observations_per_update": round(float(np.mean(obs)), 1),
         "roofline": {"kernel": "k_fusion", "bound": "hbm", "achieved": round(achieved, 2),
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic("k_fusion"),
+                     "traffic_source": "profiles/ncu_traffic.json (ncu --set full, one launch)",
                      "bytes_per_update": float(np.mean(fusion_bytes))},
         "gpu_launches": int(launches),
         "clocks": clocks,
