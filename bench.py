@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--solver-path", default="auto",
+                    choices=["auto", "resident", "resident2r", "streaming"],
+                    help="PCG data path (dfuse_ctx_set_solver_path); auto is the product default")
     return ap.parse_args()
 
 
@@ -278,6 +281,7 @@ def main():
     seq = synth.make_sequence(spec, args.seed + 1000 * rank)
     cfg = solver_cfg(spec, args.regime)
     ctx = api.context(device)
+    ctx.set_solver_path(args.solver_path)
     kf = api.Keyframe(ctx, spec.camera(), seq.I0, seq.pred, 0.02)
     geoms = [ctx.api.make_epipolar_geometry(synth.IDENTITY_Q, np.zeros(3), q, t, spec.camera())
              for (q, t, _) in seq.frames]
@@ -378,7 +382,8 @@ def main():
         "data": "synthetic (seeded Perlin-textured planes; BASELINE C2 shapes/distributions)",
         "config": {"workload": f"{spec.name}: {spec.width}x{spec.height} keyframe, {nF} tracked "
                                f"frames (reset after the last), solver {args.regime}",
-                   "regime": args.regime, "gn_iterations": cfg.gn_iterations,
+                   "regime": args.regime, "solver_path": args.solver_path,
+                   "gn_iterations": cfg.gn_iterations,
                    "cg_tol": cfg.cg_tol, "cg_max_iters": cfg.cg_max_iters,
                    "parallelism": f"replicas x{ws} (independent keyframes)",
                    "l2": "flushed before every step (512 MiB write)"},

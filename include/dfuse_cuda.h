@@ -150,13 +150,16 @@ int dfuse_ctx_destroy(dfuse_ctx* ctx);
 const char* dfuse_last_error(const dfuse_ctx* ctx);
 /* number of persistent CTAs the fusion solver uses (0 = one per SM) */
 int dfuse_ctx_set_solver_ctas(dfuse_ctx* ctx, int ctas);
-/* PCG data path: 0 = auto (SM-resident tiles when the raster fits on chip,
- * else streaming from L2/HBM), 1 = always streaming */
+/* PCG data path: 0 = auto (SM-resident tiles with one grid all-reduce per
+ * iteration when the raster fits on chip, else streaming from L2/HBM),
+ * 1 = always streaming, 2 = SM-resident with two all-reduces per iteration
+ * (the reference's direct p.q; A/B partner of 0) */
 int dfuse_ctx_set_solver_path(dfuse_ctx* ctx, int path);
 /* kernels launched on this context since creation (evidence counter) */
 int64_t dfuse_ctx_launch_count(const dfuse_ctx* ctx);
 /* diagnostics: device time (ms) of one cooperative launch running n grid-wide
- * all-reduces of the fusion solver on `grid` CTAs (variant 1 = production) */
+ * all-reduces of the fusion solver on `grid` CTAs (variant 10 = production LL
+ * all-to-all, 2 = atomic arrival counter) */
 int dfuse_debug_sync_bench(dfuse_ctx* ctx, int n, int variant, int grid, float* ms);
 /* the context's cudaStream_t (for timing with events on the launch stream) */
 void* dfuse_ctx_stream(const dfuse_ctx* ctx);

@@ -23,7 +23,7 @@ from ._ffi import (Bindings, DfuseError, EpiGeom, FrameResultC, Intrinsics, Pred
                    _f64, _mode)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdfuse_cuda.so")
+LIB_PATH = os.environ.get("DFUSE_LIB") or os.path.join(HERE, "libdfuse_cuda.so")
 
 _lib = None
 _default = {}
@@ -76,12 +76,18 @@ class Context:
     def set_solver_ctas(self, n: int) -> None:
         lib().dfuse_ctx_set_solver_ctas(self.handle, int(n))
 
-    def set_solver_path(self, streaming: bool) -> None:
-        """False: SM-resident PCG when the raster fits on chip (default);
-        True: always the streaming PCG."""
+    SOLVER_PATHS = {"auto": 0, "resident": 0, "streaming": 1, "resident2r": 2}
+
+    def set_solver_path(self, path) -> None:
+        """"auto"/"resident" (or False): SM-resident PCG with one all-reduce
+        per iteration when the raster fits on chip (default); "streaming" (or
+        True): always the streaming PCG; "resident2r": SM-resident with the
+        reference's direct p.q (two all-reduces per iteration)."""
+        if isinstance(path, bool):
+            path = "streaming" if path else "auto"
         L = lib()
         L.dfuse_ctx_set_solver_path.argtypes = [C.c_void_p, C.c_int]
-        rc = L.dfuse_ctx_set_solver_path(self.handle, 1 if streaming else 0)
+        rc = L.dfuse_ctx_set_solver_path(self.handle, self.SOLVER_PATHS[path])
         if rc:
             raise DfuseError(rc, "dfuse_ctx_set_solver_path")
 

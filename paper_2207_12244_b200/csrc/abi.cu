@@ -262,6 +262,10 @@ int dfuse_ctx_create(int device, dfuse_ctx** out) {
   ctx->num_sms = prop.multiProcessorCount;
   const char* tr = getenv("DFUSE_TRACE");
   ctx->trace = tr ? atoi(tr) : 0;
+  if (const char* rp = getenv("DFUSE_PCG_REPEAT")) {
+    ctx->diag_repeat = atoi(rp);
+    ctx->diag_sweep = strchr(rp, ',') ? atoi(strchr(rp, ',') + 1) : 0;
+  }
   if (cudaSetDevice(device) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete ctx;
@@ -304,7 +308,7 @@ int dfuse_debug_sync_bench(dfuse_ctx* ctx, int n, int variant, int grid, float* 
 }
 
 int dfuse_ctx_set_solver_path(dfuse_ctx* ctx, int path) {
-  if (!ctx || path < 0 || path > 1) return DFUSE_E_INVALID_ARGUMENT;
+  if (!ctx || path < 0 || path > 2) return DFUSE_E_INVALID_ARGUMENT;
   ctx->force_streaming = path;
   return DFUSE_OK;
 }

@@ -30,6 +30,7 @@ struct dfuse_ctx {
   int device = 0;
   int num_sms = 0;
   int solver_ctas = 0;  // 0 = auto (one per SM)
+  int diag_repeat = 0, diag_sweep = 0;  // DFUSE_PCG_REPEAT=n[,1] (diagnostics)
   int force_streaming = 0;  // 1: never use the SM-resident PCG
   int trace = 0;            // DFUSE_TRACE=1: print per-phase PCG cycle counts
   cudaStream_t stream = nullptr;

@@ -41,6 +41,7 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <climits>
 #include <vector>
 
 #include "common.cuh"
@@ -50,9 +51,6 @@ namespace dfuse_cuda {
 
 constexpr int FT = 512;  // threads per CTA (one CTA per SM)
 constexpr int FW = FT / 32;
-// each lane polls <= 5 CTA slots (grids up to 160 CTAs: B200 has 148 SMs);
-// the unrolled poll keeps all of them in flight, so this bounds registers
-constexpr int kMaxPollSlots = 5;
 
 struct Sel {
   bool net, grad, scale;
@@ -148,142 +146,167 @@ __device__ __forceinline__ double ll_wait(const unsigned long long* p, unsigned 
 // ---------------------------------------------------------------------------
 // grid all-reduce
 struct GridCtx {
-  ReduceSlot* slots;  // [2][G] 64-byte slots (+1 for the atomic variant)
+  ReduceSlot* slots;  // LL slot array (fusion_slots_bytes)
   unsigned G;
-  unsigned long long base_tag;  // tag variant only
+  unsigned long long base_tag;  // atomic-counter microbenchmark variant only
   unsigned phase;
   int syncs;
   unsigned ll_next;  // next free LL flag for the resident PCG halo exchange
 };
 
-// Sum v[0..NV) (NV <= 4) over every thread of the grid; identical bits in
-// every thread. FENCE: also order every global write made before the call
-// before every global read after it, grid-wide (needed whenever other CTAs
-// read data this CTA wrote). VARIANT 10 = LL all-to-all (production);
-// 1 = tag + acquire slots, 2 = atomic arrival counter (sync microbenchmark).
-template <int NV, bool FENCE = true, int VARIANT = 10>
-__device__ void grid_allreduce(GridCtx& c, double (&v)[NV]) {
-  __shared__ double red[FW][4];
-  __shared__ double bcast[4];
+// LL all-reduce slots: value k of CTA b in phase parity q is one 16-byte
+// {low, high} LL pair at its own 256-byte stride (the L2 hashes 256-byte
+// granules over its slices; every CTA polls every slot).
+constexpr int kSlotWords = 32;  // 256 bytes
+__device__ __forceinline__ unsigned long long* ll_slot(const GridCtx& c, unsigned phase, int k,
+                                                       unsigned b) {
+  return reinterpret_cast<unsigned long long*>(c.slots) +
+         (((size_t)(phase & 1) * 4 + k) * c.G + b) * kSlotWords;
+}
+
+// CTA-local first stage: every thread's v summed in a fixed order; the
+// result is valid in warp 0 (returned in t)
+template <int NV>
+__device__ __forceinline__ void cta_partial(double (&v)[NV], double (&t)[NV], double* red) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
   if (lane == 0)
 #pragma unroll
-    for (int k = 0; k < NV; ++k) red[wid][k] = v[k];
+    for (int k = 0; k < NV; ++k) red[wid * 4 + k] = v[k];
   __syncthreads();
-  if (wid == 0) {
-    double t[NV];
+  if (wid == 0)
 #pragma unroll
-    for (int k = 0; k < NV; ++k) t[k] = warp_sum(lane < FW ? red[lane][k] : 0.0);
-    double acc[NV];
+    for (int k = 0; k < NV; ++k) t[k] = warp_sum(lane < FW ? red[lane * 4 + k] : 0.0);
+}
+
+// warp 0 posts the CTA's partials: lane k stores value k as one LL pair
+template <int NV>
+__device__ __forceinline__ void ll_publish(const GridCtx& c, const double (&t)[NV]) {
+  const int lane = threadIdx.x & 31;
+  if (lane < NV) {
+    double tk = t[0];
+#pragma unroll
+    for (int k = 1; k < NV; ++k)
+      if (lane == k) tk = t[k];
+    st_relaxed_v2(ll_slot(c, c.phase, lane, blockIdx.x), ll_word(tk, 0, c.phase + 1),
+                  ll_word(tk, 1, c.phase + 1));
+  }
+}
+
+// Warps 0..kPollWarps-1 poll the slots: lane l of warp w owns slot
+// b = l + 32 (w + kPollWarps m). Each round loads all of the lane's slots at
+// once and sums them speculatively; the round whose flags all match wins.
+// A round's latency grows with the loads per lane, so the slots are spread
+// over several warps (one slot per lane at G <= 32 kPollWarps). Measured at
+// G = 148: one polling warp (5 slots per lane) 3.7 us per PCG all-reduce,
+// five warps 1.7 us; all 16 warps with one (slot, value) pair per lane is
+// slower again (the final barrier waits on more warps). Per-warp sums land in
+// pol[w][k]; poll_total adds them in warp order (same bits in every CTA).
+constexpr int kPollWarps = 5;
+constexpr int kMaxPollSlots = 2;  // slots per lane: grids up to 32*5*2 = 320 CTAs
+template <int NV, bool FENCE>
+__device__ __forceinline__ void ll_poll(const GridCtx& c, double* pol, long long* rec) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (wid >= kPollWarps) return;
+  const unsigned flag = c.phase + 1;
+  double acc[NV];
+  for (;;) {
+    bool ok = true;
 #pragma unroll
     for (int k = 0; k < NV; ++k) acc[k] = 0.0;
-    if (VARIANT == 13) {
-      // microbenchmark only: the CTA-local part of the all-reduce (no exchange)
 #pragma unroll
-      for (int k = 0; k < NV; ++k) acc[k] = lane == 0 ? t[k] : 0.0;
-    } else if (VARIANT == 10 || VARIANT == 12 || VARIANT == 14 || VARIANT == 15) {
-      constexpr int NW = 2 * NV;
-      const unsigned flag = c.phase + 1;
-      // parity buffers: a CTA may publish phase k+1 while a slow CTA still
-      // polls its phase-k words
-      unsigned long long* ll =
-          reinterpret_cast<unsigned long long*>(c.slots) + (size_t)(c.phase & 1) * c.G * 8;
-      if (lane < (VARIANT == 12 ? NW : NV)) {
-        double tk = t[0];
-        const int kk = VARIANT == 12 ? (lane >> 1) : lane;
+    for (int m = 0; m < kMaxPollSlots; ++m) {
+      const unsigned b = lane + 32 * (wid + kPollWarps * m);
+      if (b < c.G) {
 #pragma unroll
-        for (int k = 1; k < NV; ++k)
-          if (kk == k) tk = t[k];
-        if (VARIANT == 12) {
-          // atomic exchange: performed at L2, no write-back buffering
-          atomicExch(ll + (size_t)blockIdx.x * 8 + lane, ll_word(tk, lane & 1, flag));
-          if (FENCE) __threadfence();
-        } else if (VARIANT == 14 || VARIANT == 15) {
-          // microbenchmark: no fence; L2-only (14) or volatile (15) 16-byte store
-          unsigned long long* dst = ll + (size_t)blockIdx.x * 8 + 2 * lane;
-          const unsigned long long w0 = ll_word(tk, 0, flag), w1 = ll_word(tk, 1, flag);
-          if (VARIANT == 14)
-            asm volatile("st.global.cg.v2.u64 [%0], {%1, %2};" ::"l"(dst), "l"(w0), "l"(w1)
-                         : "memory");
-          else
-            asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(dst), "l"(w0),
-                         "l"(w1)
-                         : "memory");
-        } else {
-          // lane k publishes value k as one 16-byte {low, high} LL pair; with
-          // FENCE the fence also publishes the CTA's earlier global writes
-          st_relaxed_v2(ll + (size_t)blockIdx.x * 8 + 2 * lane, ll_word(tk, 0, flag),
-                        ll_word(tk, 1, flag));
-          if (FENCE) __threadfence();
+        for (int k = 0; k < NV; ++k) {
+          unsigned long long w0, w1;
+          ld_relaxed_v2(ll_slot(c, c.phase, k, b), w0, w1);
+          ok &= (unsigned)(w0 >> 32) == flag && (unsigned)(w1 >> 32) == flag;
+          acc[k] += ll_value(w0, w1);
         }
       }
-      // every round loads all of this lane's slots at once and sums them
-      // speculatively (fixed order); the round whose flags all match wins
-      for (;;) {
-        bool ok = true;
-        double accr[NV];
+    }
+    if (rec && threadIdx.x == 0) rec[3] += 1;  // diagnostics: poll rounds of warp 0
+    if (__all_sync(0xffffffffu, ok)) break;
+  }
+  if (FENCE) __threadfence();
 #pragma unroll
-        for (int k = 0; k < NV; ++k) accr[k] = 0.0;
+  for (int k = 0; k < NV; ++k) acc[k] = warp_sum(acc[k]);
+  if (lane == 0)
 #pragma unroll
-        for (int m = 0; m < kMaxPollSlots; ++m) {
-          const unsigned b = lane + 32 * m;
-          if (b < c.G) {
+    for (int k = 0; k < NV; ++k) pol[wid * 4 + k] = acc[k];
+}
+
+template <int NV>
+__device__ __forceinline__ void poll_total(const double* pol, double (&v)[NV]) {
 #pragma unroll
-            for (int k = 0; k < NV; ++k) {
-              unsigned long long w0, w1;
-              ld_relaxed_v2(ll + (size_t)b * 8 + 2 * k, w0, w1);
-              ok &= (unsigned)(w0 >> 32) == flag && (unsigned)(w1 >> 32) == flag;
-              accr[k] += ll_value(w0, w1);
-            }
-          }
-        }
-        if (__all_sync(0xffffffffu, ok)) {
+  for (int k = 0; k < NV; ++k) {
+    double s = pol[k];
 #pragma unroll
-          for (int k = 0; k < NV; ++k) acc[k] = accr[k];
-          break;
-        }
-      }
+    for (int w = 1; w < kPollWarps; ++w) s += pol[w * 4 + k];
+    v[k] = s;
+  }
+}
+
+// Sum v[0..NV) (NV <= 4) over every thread of the grid; identical bits in
+// every thread (every CTA adds the same partials in the same order).
+// FENCE: also order every global write made before the call before every
+// global read after it, grid-wide (needed whenever other CTAs read data this
+// CTA wrote). VARIANT 10 = LL all-to-all (production); 2 = atomic arrival
+// counter (sync microbenchmark baseline). rec: DFUSE_TRACE=3 timestamps.
+template <int NV, bool FENCE = true, int VARIANT = 10>
+__device__ void grid_allreduce(GridCtx& c, double (&v)[NV], long long* rec = nullptr) {
+  __shared__ double red[FW * 4];
+  __shared__ double pol[kPollWarps * 4];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (rec && threadIdx.x == 0) rec[0] = clock64();
+  double t[NV];
+  cta_partial(v, t, red);
+  if (VARIANT == 10) {
+    if (wid == 0) {
+      // release: the CTA's earlier global writes (ordered before this point
+      // by the barrier in cta_partial) become visible before the LL words
       if (FENCE) __threadfence();
-    } else {
-      const unsigned long long tag = c.base_tag + c.phase + 1;
-      ReduceSlot* buf = c.slots + (size_t)(c.phase & 1) * c.G;
+      if (rec && lane == 0) rec[1] = clock64();
+      ll_publish(c, t);
+    }
+    ll_poll<NV, FENCE>(c, pol, rec);
+    if (rec && threadIdx.x == 0) rec[2] = clock64();
+    __syncthreads();
+    poll_total(pol, v);
+  } else {
+    ReduceSlot* buf = c.slots + (size_t)(c.phase & 1) * c.G;
+    if (wid == 0) {
       if (lane == 0) {
 #pragma unroll
         for (int k = 0; k < NV; ++k) buf[blockIdx.x].v[k] = t[k];
-        if (VARIANT == 2) {
-          __threadfence();
-          atomicAdd(reinterpret_cast<unsigned*>(c.slots + 2 * c.G), 1u);
-        } else {
-          st_release_u64(&buf[blockIdx.x].tag, tag);
+        __threadfence();
+        atomicAdd(reinterpret_cast<unsigned*>(c.slots + 2 * c.G), 1u);
+        const unsigned target = (c.phase + 1) * c.G;
+        while (ld_acquire(reinterpret_cast<unsigned*>(c.slots + 2 * c.G)) < target) {
         }
       }
-      if (VARIANT == 2) {
-        const unsigned target = (c.phase + 1) * c.G;
-        if (lane == 0)
-          while (ld_acquire(reinterpret_cast<unsigned*>(c.slots + 2 * c.G)) < target) {
-          }
-        __syncwarp();
-      } else {
-        for (unsigned b = lane; b < c.G; b += 32)
-          while (ld_acquire_u64(&buf[b].tag) != tag) {
-          }
-      }
+      __syncwarp();
       __threadfence();
+      double acc[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) acc[k] = 0.0;
       for (unsigned b = lane; b < c.G; b += 32)
 #pragma unroll
         for (int k = 0; k < NV; ++k) acc[k] += __ldcg(&buf[b].v[k]);
+#pragma unroll
+      for (int k = 0; k < NV; ++k) acc[k] = warp_sum(acc[k]);
+      if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) pol[k] = acc[k];
     }
+    __syncthreads();
 #pragma unroll
-    for (int k = 0; k < NV; ++k) acc[k] = warp_sum(acc[k]);
-    if (lane == 0)
-#pragma unroll
-      for (int k = 0; k < NV; ++k) bcast[k] = acc[k];
+    for (int k = 0; k < NV; ++k) v[k] = pol[k];
   }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < NV; ++k) v[k] = bcast[k];
+  if (rec && threadIdx.x == 0) rec[4] = clock64();
   c.phase += 1;
   c.syncs += 1;
 }
@@ -298,80 +321,23 @@ __device__ __forceinline__ void grid_sync(GridCtx& c) {
 // runs its next SpMV there) before wait() collects the grid sum. No other
 // all-reduce may run in between.
 __device__ __forceinline__ double* split_smem() {
-  __shared__ double s[FW * 4 + 4];
+  __shared__ double s[FW * 4 + kPollWarps * 4];
   return s;
 }
 
 template <int NV>
 __device__ void grid_allreduce_publish(GridCtx& c, double (&v)[NV]) {
-  double* red = split_smem();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < NV; ++k) red[wid * 4 + k] = v[k];
-  __syncthreads();
-  if (wid == 0) {
-    double t[NV];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) t[k] = warp_sum(lane < FW ? red[lane * 4 + k] : 0.0);
-    const unsigned flag = c.phase + 1;
-    unsigned long long* ll =
-        reinterpret_cast<unsigned long long*>(c.slots) + (size_t)(c.phase & 1) * c.G * 8;
-    if (lane < NV) {
-      double tk = t[0];
-#pragma unroll
-      for (int k = 1; k < NV; ++k)
-        if (lane == k) tk = t[k];
-      st_relaxed_v2(ll + (size_t)blockIdx.x * 8 + 2 * lane, ll_word(tk, 0, flag),
-                    ll_word(tk, 1, flag));
-    }
-  }
+  double t[NV];
+  cta_partial(v, t, split_smem());
+  if ((threadIdx.x >> 5) == 0) ll_publish(c, t);
 }
 
 template <int NV>
 __device__ void grid_allreduce_wait(GridCtx& c, double (&v)[NV]) {
-  double* bc = split_smem() + FW * 4;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (wid == 0) {
-    const unsigned flag = c.phase + 1;
-    const unsigned long long* ll =
-        reinterpret_cast<unsigned long long*>(c.slots) + (size_t)(c.phase & 1) * c.G * 8;
-    double acc[NV];
-    for (;;) {
-      bool ok = true;
-      double accr[NV];
-#pragma unroll
-      for (int k = 0; k < NV; ++k) accr[k] = 0.0;
-#pragma unroll
-      for (int m = 0; m < kMaxPollSlots; ++m) {
-        const unsigned b = lane + 32 * m;
-        if (b < c.G) {
-#pragma unroll
-          for (int k = 0; k < NV; ++k) {
-            unsigned long long w0, w1;
-            ld_relaxed_v2(ll + (size_t)b * 8 + 2 * k, w0, w1);
-            ok &= (unsigned)(w0 >> 32) == flag && (unsigned)(w1 >> 32) == flag;
-            accr[k] += ll_value(w0, w1);
-          }
-        }
-      }
-      if (__all_sync(0xffffffffu, ok)) {
-#pragma unroll
-        for (int k = 0; k < NV; ++k) acc[k] = accr[k];
-        break;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < NV; ++k) acc[k] = warp_sum(acc[k]);
-    if (lane == 0)
-#pragma unroll
-      for (int k = 0; k < NV; ++k) bc[k] = acc[k];
-  }
+  double* pol = split_smem() + FW * 4;
+  ll_poll<NV, false>(c, pol, nullptr);
   __syncthreads();
-#pragma unroll
-  for (int k = 0; k < NV; ++k) v[k] = bc[k];
+  poll_total(pol, v);
   c.phase += 1;
   c.syncs += 1;
 }
@@ -668,16 +634,8 @@ __device__ int pcg_stream(GridCtx& c, const FusionArgs& a, const Range& rg, doub
 }
 
 // ---------------------------------------------------------------------------
-// SM-resident PCG (same iteration as pcg_stream, same stop rules, same
-// per-pixel expressions). CTA b owns tile b of a tiles_x x tiles_y partition.
-// x, r and z = r/diag live in registers (PPT pixels per thread);
-// diag / right / down and p with a one-pixel halo in shared memory. Per
-// iteration only the tile boundary leaves the SM: each CTA publishes its
-// boundary z (after sweep B) and p (sweep A, parity buffer) as LL words in
-// raster-indexed arrays, and rebuilds its halo p = z + beta p_prev from the
-// neighbours' words -- the owner's own expression on the owner's own bits,
-// so halo and owner values agree exactly. The LL flags order the halo data,
-// so the two all-reduces per iteration need no memory fence.
+// SM-resident PCG tiling (pcg_tile.cuh): CTA b owns tile b of a
+// tiles_x x tiles_y partition of the raster.
 struct TileGeo {
   int x0, y0, tw, th;  // tw*th == 0 for CTAs without a tile
 };
@@ -695,204 +653,14 @@ __device__ __forceinline__ TileGeo my_tile(const FusionArgs& a) {
   return t;
 }
 
-template <int PPT>
-__device__ int pcg_resident_v1(GridCtx& c, const FusionArgs& a, double bnorm2, double rz,
-                               int* its) {
-  extern __shared__ double dsm[];
-  const TileGeo tg = my_tile(a);
-  const int T = tg.tw * tg.th;
-  constexpr int TC = PPT * FT;  // tile capacity
-  double* s_diag = dsm;
-  double* s_right = dsm + TC;
-  double* s_down = dsm + 2 * TC;
-  double* s_q = dsm + 3 * TC;
-  double* s_p = dsm + 4 * TC;                                // (th+2) x (tw+2), halo included
-  double* s_hright = s_p + (a.th_max + 2) * (a.tw_max + 2);  // right[] of the left halo column
-  double* s_hdown = s_hright + a.th_max;                     // down[] of the top halo row
-  const int W = a.W, H = a.H, pw = tg.tw + 2;
-  const long P = (long)W * H;
-  unsigned long long* z_ll = a.halo;  // [P][2]
-  unsigned long long* p_ll[2] = {a.halo + 2 * P, a.halo + 4 * P};
-  // LL flags of this solve: z version v -> base + v; p of iteration it -> base + it + 1
-  const unsigned base = c.ll_next;
-  c.ll_next += (unsigned)a.cg_max + 2u;
-
-  double xr[PPT], rr_[PPT], zr[PPT];
-  int gi_[PPT];  // global pixel index, -1 if none
-  bool bd_[PPT];  // on the tile boundary
-#pragma unroll
-  for (int j = 0; j < PPT; ++j) {
-    const int k = threadIdx.x + FT * j;
-    xr[j] = rr_[j] = zr[j] = 0.0;
-    gi_[j] = -1;
-    bd_[j] = false;
-    if (k < T) {
-      const int ly = k / tg.tw, lx = k - ly * tg.tw;
-      const int gi = (tg.y0 + ly) * W + tg.x0 + lx;
-      gi_[j] = gi;
-      bd_[j] = lx == 0 || ly == 0 || lx == tg.tw - 1 || ly == tg.th - 1;
-      const double d = __ldcg(a.diag + gi);
-      s_diag[k] = d;
-      s_right[k] = __ldcg(a.right + gi);
-      s_down[k] = __ldcg(a.down + gi);
-      rr_[j] = __ldcg(a.r + gi);
-      zr[j] = rr_[j] / d;  // z = r/diag, fusion.hpp:329
-      if (bd_[j]) ll_store(z_ll + 2 * (long)gi, zr[j], base + 1);
-    }
-  }
-  for (int t = threadIdx.x; t < tg.th; t += FT)
-    s_hright[t] = tg.x0 > 0 ? __ldcg(a.right + (tg.y0 + t) * W + tg.x0 - 1) : 0.0;
-  for (int t = threadIdx.x; t < tg.tw; t += FT)
-    s_hdown[t] = tg.y0 > 0 ? __ldcg(a.down + (tg.y0 - 1) * W + tg.x0 + t) : 0.0;
-
-  const int ring_n = T > 0 ? 2 * (tg.tw + tg.th) : 0;
-  const double tol2 = a.cg_tol * a.cg_tol * bnorm2;
-  double prev = bnorm2, beta = 0.0;
-  int streak = 0, status = 0;
-  *its = 0;
-  // DFUSE_TRACE: CTA 0 / thread 0 accumulates SM cycles per phase
-  const bool tracer = a.trace && blockIdx.x == 0 && threadIdx.x == 0;
-  long long tr[6] = {0, 0, 0, 0, 0, 0}, t_last = tracer ? df_now() : 0;
-#define DF_TRACE(k)                 \
-  if (tracer) {                     \
-    const long long t_ = df_now(); \
-    tr[k] += t_ - t_last;           \
-    t_last = t_;                    \
-  }
-  for (int it = 0; it < a.cg_max; ++it) {
-    *its = it + 1;
-    const bool first = it == 0;
-    // ---- sweep A: halo ring p = z + beta p_prev from the neighbours' LL words
-    for (int t = threadIdx.x; t < ring_n; t += FT) {
-      int gx, gy, so;
-      if (t < tg.tw) {
-        gx = tg.x0 + t, gy = tg.y0 - 1, so = t + 1;
-      } else if (t < 2 * tg.tw) {
-        gx = tg.x0 + t - tg.tw, gy = tg.y0 + tg.th, so = (tg.th + 1) * pw + t - tg.tw + 1;
-      } else if (t < 2 * tg.tw + tg.th) {
-        gx = tg.x0 - 1, gy = tg.y0 + t - 2 * tg.tw, so = (t - 2 * tg.tw + 1) * pw;
-      } else {
-        gx = tg.x0 + tg.tw, gy = tg.y0 + t - 2 * tg.tw - tg.th,
-        so = (t - 2 * tg.tw - tg.th + 1) * pw + tg.tw + 1;
-      }
-      if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
-        const long j = (long)gy * W + gx;
-        const unsigned fz = base + (first ? 1u : (unsigned)it + 1u), fp = base + (unsigned)it;
-        const unsigned long long* zw = z_ll + 2 * j;
-        const unsigned long long* pw_ = p_ll[(it + 1) & 1] + 2 * j;
-        unsigned long long z0, z1, p0 = (unsigned long long)fp << 32, p1 = p0;
-        for (;;) {  // all four words in flight per round
-          z0 = ld_relaxed_u64(zw);
-          z1 = ld_relaxed_u64(zw + 1);
-          if (!first) {
-            p0 = ld_relaxed_u64(pw_);
-            p1 = ld_relaxed_u64(pw_ + 1);
-          }
-          if ((unsigned)(z0 >> 32) == fz && (unsigned)(z1 >> 32) == fz &&
-              (unsigned)(p0 >> 32) == fp && (unsigned)(p1 >> 32) == fp)
-            break;
-        }
-        const double z = ll_value(z0, z1);
-        s_p[so] = first ? z : z + beta * ll_value(p0, p1);
-      }
-    }
-    DF_TRACE(0);
-    // own p = z + beta p (fusion.hpp:360,365; p = z at it 0, fusion.hpp:329-330)
-#pragma unroll
-    for (int j = 0; j < PPT; ++j) {
-      const int k = threadIdx.x + FT * j;
-      if (k < T) {
-        const int ly = k / tg.tw, lx = k - ly * tg.tw;
-        const int so = (ly + 1) * pw + lx + 1;
-        const double p = first ? zr[j] : zr[j] + beta * s_p[so];
-        s_p[so] = p;
-        if (bd_[j]) ll_store(p_ll[it & 1] + 2 * (long)gi_[j], p, base + (unsigned)it + 1u);
-      }
-    }
-    __syncthreads();
-    DF_TRACE(1);
-    // q = H p, StencilMatrix::apply order (fusion.hpp:127-131)
-    double pq = 0.0;
-#pragma unroll
-    for (int j = 0; j < PPT; ++j) {
-      const int k = threadIdx.x + FT * j;
-      if (k < T) {
-        const int ly = k / tg.tw, lx = k - ly * tg.tw;
-        const int so = (ly + 1) * pw + lx + 1;
-        const int gx = tg.x0 + lx, gy = tg.y0 + ly;
-        const double pi = s_p[so];
-        double v = s_diag[k] * pi;
-        if (gx + 1 < W) v += s_right[k] * s_p[so + 1];
-        if (gx > 0) v += (lx > 0 ? s_right[k - 1] : s_hright[ly]) * s_p[so - 1];
-        if (gy + 1 < H) v += s_down[k] * s_p[so + pw];
-        if (gy > 0) v += (ly > 0 ? s_down[k - tg.tw] : s_hdown[lx]) * s_p[so - pw];
-        s_q[k] = v;
-        pq += pi * v;
-      }
-    }
-    DF_TRACE(2);
-    double v1[1] = {pq};
-    grid_allreduce<1, false>(c, v1);
-    DF_TRACE(3);
-    if (!(v1[0] > 0.0)) {
-      status = DFUSE_E_CG_DIVERGENCE;
-      break;
-    }
-    const double alpha = rz / v1[0];
-    // ---- sweep B (fusion.hpp:345-362)
-    double rr = 0.0, rzn = 0.0;
-#pragma unroll
-    for (int j = 0; j < PPT; ++j) {
-      const int k = threadIdx.x + FT * j;
-      if (k < T) {
-        const int ly = k / tg.tw, lx = k - ly * tg.tw;
-        const int so = (ly + 1) * pw + lx + 1;
-        xr[j] = xr[j] + alpha * s_p[so];
-        const double r = rr_[j] - alpha * s_q[k];
-        rr_[j] = r;
-        rr += r * r;
-        const double z = r / s_diag[k];
-        zr[j] = z;
-        rzn += r * z;
-        if (bd_[j]) ll_store(z_ll + 2 * (long)gi_[j], z, base + (unsigned)it + 2u);
-      }
-    }
-    DF_TRACE(4);
-    double v2[2] = {rr, rzn};
-    grid_allreduce<2, false>(c, v2);
-    DF_TRACE(5);
-    const double rn = v2[0];
-    if (rn <= tol2) break;
-    if (rn > prev) {
-      if (++streak >= 10) {
-        status = DFUSE_E_CG_DIVERGENCE;
-        break;
-      }
-    } else {
-      streak = 0;
-    }
-    prev = rn;
-    beta = v2[1] / rz;
-    rz = v2[1];
-  }
-#undef DF_TRACE
-  if (tracer)
-    for (int k = 0; k < 6; ++k) a.ctl->trace[k] += tr[k];
-  // delta to the raster for the line search (x == 0 if no iteration ran)
-#pragma unroll
-  for (int j = 0; j < PPT; ++j)
-    if (gi_[j] >= 0) a.x[gi_[j]] = xr[j];
-  grid_sync(c);  // fenced: the trial sweeps read x at the neighbours
-  return status;
-}
-
 #include "pcg_tile.cuh"
 
 template <int PPT>
 __device__ __forceinline__ int pcg_solve(GridCtx& c, const FusionArgs& a, const Range& rg,
                                          double bnorm2, double rz, int* its) {
   if constexpr (PPT > 0) {
-    return pcg_resident<PPT>(c, a, bnorm2, rz, its);
+    return a.pcg_2r ? pcg_resident_2r<PPT>(c, a, bnorm2, rz, its)
+                    : pcg_resident<PPT>(c, a, bnorm2, rz, its);
   } else {
     const int st = pcg_stream(c, a, rg, bnorm2, rz, its);
     if (*its == 0) {
@@ -953,6 +721,16 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
       status = DFUSE_E_CG_DIVERGENCE;
     } else {
       status = pcg_solve<PPT>(c, a, rg, w[0], w[1], &its);
+      // diagnostics (DFUSE_PCG_REPEAT=n[,sweep]): solve the same system n-1
+      // more times in this launch, optionally after a streaming sweep
+      for (int rep = 1; rep < a.diag_repeat && status == 0; ++rep) {
+        if (a.diag_sweep) {
+          for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT)
+            a.q[i] = a.diag[i] * a.right[i] + a.down[i] * a.b[i];
+          grid_sync(c);
+        }
+        status = pcg_solve<PPT>(c, a, rg, w[0], w[1], &its);
+      }
     }
     if (leader) ctl->pcg_last = its;
   } else {  // OP_OPTIMIZE, fusion.hpp:402-454
@@ -1185,7 +963,7 @@ __global__ void __launch_bounds__(FT, 1) k_sync_bench(ReduceSlot* slots, unsigne
   double acc = 0.0;
   for (int i = 0; i < n; ++i) {
     double v[2] = {1.0, (double)threadIdx.x};
-    grid_allreduce<2, VARIANT < 10, VARIANT>(c, v);
+    grid_allreduce<2, VARIANT != 10, VARIANT>(c, v);
     acc += v[0];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *out = acc;
@@ -1216,11 +994,17 @@ int fusion_grid(dfuse_ctx* ctx) {
   }
   int g = ctx->solver_ctas > 0 ? ctx->solver_ctas : ctx->num_sms;
   if (g > ctx->num_sms) g = ctx->num_sms;  // one CTA per SM: resident tiles need the SM's smem
-  if (g > 32 * kMaxPollSlots) g = 32 * kMaxPollSlots;
+  if (g > 32 * kPollWarps * kMaxPollSlots) g = 32 * kPollWarps * kMaxPollSlots;
   return g;
 }
 
-size_t fusion_slots_bytes(int grid) { return sizeof(ReduceSlot) * (2 * (size_t)grid + 1); }
+size_t fusion_slots_bytes(int grid) {
+  // LL slots (2 parities x 4 values x grid x 256 B) or the atomic-counter
+  // microbenchmark variants' ReduceSlots, whichever is larger
+  const size_t ll = sizeof(unsigned long long) * kSlotWords * 8 * (size_t)grid;
+  const size_t tag = sizeof(ReduceSlot) * (2 * (size_t)grid + 1);
+  return ll > tag ? ll : tag;
+}
 
 size_t fusion_halo_bytes(long P) { return sizeof(unsigned long long) * 6 * (size_t)P; }
 
@@ -1276,7 +1060,8 @@ static void launch_fusion_t(dfuse_ctx* ctx, FusionArgs& a, int grid) {
 
 void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
   plan_tiles(a, grid);
-  if (ctx->force_streaming) a.ppt = 0;
+  if (ctx->force_streaming == 1) a.ppt = 0;
+  a.pcg_2r = ctx->force_streaming == 2;
   {  // scale-round staging lives in the resident PCG's shared memory
     const long range = ((long)a.W * a.H + grid - 1) / grid;
     a.stage_n = (a.ppt > 0 && (size_t)(16 * range) <= pcg_tile_smem(a.tw_max, a.th_max))
@@ -1289,10 +1074,13 @@ void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
   if (a.ppt > 0)
     DF_CUDA(cudaMemsetAsync(a.halo, 0, fusion_halo_bytes((long)a.W * a.H), ctx->stream));
   a.trace = ctx->trace;
+  a.diag_repeat = ctx->diag_repeat;
+  a.diag_sweep = ctx->diag_sweep;
   a.dbg = nullptr;
+  const size_t dbg_n = ctx->trace >= 3 ? (size_t)256 * grid * 8 : (size_t)8 * grid;
   if (ctx->trace >= 2) {
-    a.dbg = (long long*)scratch(ctx, S_TMP4, sizeof(long long) * 8 * grid);
-    DF_CUDA(cudaMemsetAsync(a.dbg, 0, sizeof(long long) * 8 * grid, ctx->stream));
+    a.dbg = (long long*)scratch(ctx, S_TMP4, sizeof(long long) * dbg_n);
+    DF_CUDA(cudaMemsetAsync(a.dbg, 0, sizeof(long long) * dbg_n, ctx->stream));
   }
   if (a.ppt == 4)
     launch_fusion_t<4>(ctx, a, grid);
@@ -1310,22 +1098,52 @@ void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
     DF_CUDA(cudaMemcpyAsync(&its, &a.ctl->stats.pcg_total, sizeof its, cudaMemcpyDeviceToHost,
                             ctx->stream));
     DF_CUDA(cudaStreamSynchronize(ctx->stream));
+    // PCG phases are SM cycles; convert with the clock measured over the solves
+    const double ghz = tr[6] > 0 ? (double)tr[7] / (double)tr[6] : 1.0;
+    double ns[6];
+    for (int k = 0; k < 6; ++k) ns[k] = (double)tr[k] / ghz;
     fprintf(stderr,
-            "dfuse trace (ppt %d, ns, CTA 0): ring %lld spmv %lld wait_rz %lld pq_upd %lld "
-            "ar_pq %lld sweepB_pub %lld | scale %lld strial %lld assemble %lld pcg %lld dtrial %lld "
+            "dfuse trace (ppt %d, ns, CTA 0): ring %.0f spmv %.0f ar/wait_rz %.0f pq_upd %.0f "
+            "ar_pq %.0f sweep %.0f | scale %lld strial %lld assemble %lld pcg %lld dtrial %lld "
             "(pcg its %d) sm_clock %.0f MHz\n",
-            a.ppt, tr[0], tr[1], tr[2], tr[3], tr[4], tr[5], tr[8], tr[9], tr[10], tr[11], tr[12],
-            tr[6] > 0 ? 1e3 * (double)tr[7] / (double)tr[6] : 0.0,
-            its);
-    if (a.dbg) {  // per-CTA spread of each phase
+            a.ppt, ns[0], ns[1], ns[2], ns[3], ns[4], ns[5], tr[8], tr[9], tr[10], tr[11], tr[12],
+            its, 1e3 * ghz);
+    if (a.dbg && ctx->trace >= 3) {  // each CTA's view of its all-reduces (SM cycles)
+      std::vector<long long> h(dbg_n);
+      DF_CUDA(cudaMemcpy(h.data(), a.dbg, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost));
+      // per CTA: mean entry->publish, publish->done, done->exit, rounds
+      std::vector<double> e2p, p2d, d2x, rounds;
+      for (int b = 0; b < grid; ++b) {
+        double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+        int n = 0;
+        for (int it = 0; it < 256; ++it) {
+          const long long* r = h.data() + ((size_t)it * grid + b) * 8;
+          if (!r[0] || !r[4]) continue;
+          s0 += r[1] - r[0]; s1 += r[2] - r[1]; s2 += r[4] - r[2]; s3 += r[3]; ++n;
+        }
+        if (!n) continue;
+        e2p.push_back(s0 / n / ghz); p2d.push_back(s1 / n / ghz); d2x.push_back(s2 / n / ghz);
+        rounds.push_back(s3 / n);
+      }
+      auto stat = [](std::vector<double> v, const char* name) {
+        if (v.empty()) return;
+        std::sort(v.begin(), v.end());
+        fprintf(stderr, "  all-reduce %s across CTAs: min %.0f median %.0f max %.0f\n", name, v[0],
+                v[v.size() / 2], v.back());
+      };
+      stat(e2p, "entry->publish ns");
+      stat(p2d, "publish->complete ns");
+      stat(d2x, "complete->exit ns");
+      stat(rounds, "poll rounds");
+    } else if (a.dbg) {  // per-CTA spread of each phase
       std::vector<long long> h((size_t)8 * grid);
       DF_CUDA(cudaMemcpy(h.data(), a.dbg, sizeof(long long) * 8 * grid, cudaMemcpyDeviceToHost));
       for (int k = 0; k < 6; ++k) {
         std::vector<long long> col(grid);
         for (int b = 0; b < grid; ++b) col[b] = h[(size_t)b * 8 + k];
         std::sort(col.begin(), col.end());
-        fprintf(stderr, "  phase %d across CTAs: min %lld median %lld max %lld\n", k, col[0],
-                col[grid / 2], col[grid - 1]);
+        fprintf(stderr, "  phase %d across CTAs (ns): min %.0f median %.0f max %.0f\n", k,
+                col[0] / ghz, col[grid / 2] / ghz, col[grid - 1] / ghz);
       }
     }
   }
@@ -1348,13 +1166,7 @@ float sync_bench(dfuse_ctx* ctx, int n, int variant, int grid) {
   DF_CUDA(cudaMemsetAsync(slots, 0, bytes, ctx->stream));
   unsigned long long tag = next_tag();
   void* args[] = {&slots, &tag, &n, &out};
-  const void* fn = variant == 1    ? (const void*)k_sync_bench<1>
-                   : variant == 2  ? (const void*)k_sync_bench<2>
-                   : variant == 12 ? (const void*)k_sync_bench<12>
-                   : variant == 13 ? (const void*)k_sync_bench<13>
-                   : variant == 14 ? (const void*)k_sync_bench<14>
-                   : variant == 15 ? (const void*)k_sync_bench<15>
-                                   : (const void*)k_sync_bench<10>;
+  const void* fn = variant == 2 ? (const void*)k_sync_bench<2> : (const void*)k_sync_bench<10>;
   DF_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
   DF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(FT), args, 0, ctx->stream));
   DF_LAUNCHED(ctx);

@@ -1,5 +1,5 @@
 """Profiling driver: one fixed-iteration PCG solve (dfuse_solve_depth_step)
-on a 640x480 system, resident path unless --streaming. Used under ncu."""
+on a 640x480 system, solver path from argv[1] (auto|resident2r|streaming). Used under ncu."""
 import os
 import sys
 
@@ -11,7 +11,7 @@ from paper_2207_12244_b200 import api  # noqa: E402
 from paper_2207_12244_b200._ffi import RobustConfig  # noqa: E402
 
 ctx = api.context(0)
-ctx.set_solver_path("--streaming" in sys.argv)
+ctx.set_solver_path(sys.argv[1] if len(sys.argv) > 1 else "auto")
 st, semi, pred = make_random_problem(5, 640, 480)
 eq = ctx.api.assemble_normal_equations(st, semi, pred)
 cfg = RobustConfig(cg_tol=0.0, cg_max_iters=int(os.environ.get("PCG_ITERS", "100")))

@@ -22,7 +22,7 @@ L = api.lib()
 L.dfuse_debug_sync_bench.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int,
                                      C.POINTER(C.c_float)]
 ms = C.c_float()
-for variant in (10, 14, 15):
+for variant in (10, 2):
     for grid in (32, 74, 148):
         t = {}
         L.dfuse_debug_sync_bench(ctx.handle, 50000, variant, grid, C.byref(ms))  # clock warm-up

@@ -23,12 +23,13 @@ pytestmark = pytest.mark.gpu
 MODES = ["full", "nopairwise", "lsscale"]
 
 
-@pytest.fixture(params=["resident", "streaming"], autouse=True)
+@pytest.fixture(params=["resident", "resident2r", "streaming"], autouse=True)
 def solver_path(request, gpu_ctx):
-    """Every test runs on both PCG data paths (SM-resident tiles / streaming)."""
-    gpu_ctx.set_solver_path(request.param == "streaming")
+    """Every test runs on every PCG data path (SM-resident tiles with one or
+    two all-reduces per iteration / streaming)."""
+    gpu_ctx.set_solver_path(request.param)
     yield request.param
-    gpu_ctx.set_solver_path(False)
+    gpu_ctx.set_solver_path("auto")
 
 
 def _problems():
