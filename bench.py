@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--solver-path", default="auto",
-                    choices=["auto", "resident", "resident2r", "streaming"],
+                    choices=["auto", "resident", "resident1r", "resident2r", "streaming"],
                     help="PCG data path (dfuse_ctx_set_solver_path); auto is the product default")
     return ap.parse_args()
 

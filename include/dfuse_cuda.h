@@ -150,10 +150,11 @@ int dfuse_ctx_destroy(dfuse_ctx* ctx);
 const char* dfuse_last_error(const dfuse_ctx* ctx);
 /* number of persistent CTAs the fusion solver uses (0 = one per SM) */
 int dfuse_ctx_set_solver_ctas(dfuse_ctx* ctx, int ctas);
-/* PCG data path: 0 = auto (SM-resident tiles with one grid all-reduce per
- * iteration when the raster fits on chip, else streaming from L2/HBM),
- * 1 = always streaming, 2 = SM-resident with two all-reduces per iteration
- * (the reference's direct p.q; A/B partner of 0) */
+/* PCG data path: 0 = auto (SM-resident tiles, pipelined PCG whose one grid
+ * all-reduce per iteration overlaps the SpMV, when the raster fits on chip,
+ * else streaming from L2/HBM), 1 = always streaming, 2 = SM-resident with
+ * two all-reduces per iteration (the reference's direct p.q), 3 = SM-resident
+ * Chronopoulos-Gear (one exposed all-reduce per iteration) */
 int dfuse_ctx_set_solver_path(dfuse_ctx* ctx, int path);
 /* kernels launched on this context since creation (evidence counter) */
 int64_t dfuse_ctx_launch_count(const dfuse_ctx* ctx);

@@ -76,13 +76,15 @@ class Context:
     def set_solver_ctas(self, n: int) -> None:
         lib().dfuse_ctx_set_solver_ctas(self.handle, int(n))
 
-    SOLVER_PATHS = {"auto": 0, "resident": 0, "streaming": 1, "resident2r": 2}
+    SOLVER_PATHS = {"auto": 0, "resident": 0, "streaming": 1, "resident2r": 2, "resident1r": 3}
 
     def set_solver_path(self, path) -> None:
-        """"auto"/"resident" (or False): SM-resident PCG with one all-reduce
-        per iteration when the raster fits on chip (default); "streaming" (or
-        True): always the streaming PCG; "resident2r": SM-resident with the
-        reference's direct p.q (two all-reduces per iteration)."""
+        """"auto"/"resident" (or False): SM-resident pipelined PCG (one
+        all-reduce per iteration, overlapped with the SpMV) when the raster
+        fits on chip (default); "streaming" (or True): always the streaming
+        PCG; "resident1r": SM-resident Chronopoulos-Gear PCG (one exposed
+        all-reduce); "resident2r": SM-resident with the reference's direct
+        p.q (two all-reduces per iteration)."""
         if isinstance(path, bool):
             path = "streaming" if path else "auto"
         L = lib()

@@ -308,7 +308,7 @@ int dfuse_debug_sync_bench(dfuse_ctx* ctx, int n, int variant, int grid, float* 
 }
 
 int dfuse_ctx_set_solver_path(dfuse_ctx* ctx, int path) {
-  if (!ctx || path < 0 || path > 2) return DFUSE_E_INVALID_ARGUMENT;
+  if (!ctx || path < 0 || path > 3) return DFUSE_E_INVALID_ARGUMENT;
   ctx->force_streaming = path;
   return DFUSE_OK;
 }

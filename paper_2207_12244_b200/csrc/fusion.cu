@@ -655,12 +655,15 @@ __device__ __forceinline__ TileGeo my_tile(const FusionArgs& a) {
 
 #include "pcg_tile.cuh"
 
-template <int PPT>
+template <int PPT, int VAR>
 __device__ __forceinline__ int pcg_solve(GridCtx& c, const FusionArgs& a, const Range& rg,
                                          double bnorm2, double rz, int* its) {
   if constexpr (PPT > 0) {
-    return a.pcg_2r ? pcg_resident_2r<PPT>(c, a, bnorm2, rz, its)
-                    : pcg_resident<PPT>(c, a, bnorm2, rz, its);
+    if constexpr (VAR == 1) return pcg_resident<PPT>(c, a, bnorm2, rz, its);
+    if constexpr (VAR == 2) return pcg_resident_2r<PPT>(c, a, bnorm2, rz, its);
+    PcgHandover h;
+    const int st = pcg_resident_pipe<PPT>(c, a, bnorm2, rz, its, &h);
+    return st >= 0 ? st : pcg_resume_cg<PPT>(c, a, bnorm2, h, its);
   } else {
     const int st = pcg_stream(c, a, rg, bnorm2, rz, its);
     if (*its == 0) {
@@ -672,7 +675,11 @@ __device__ __forceinline__ int pcg_solve(GridCtx& c, const FusionArgs& a, const 
 }
 
 // ---------------------------------------------------------------------------
-template <int PPT>
+// PPT: pixels per thread of the SM-resident PCG (0 = streaming PCG);
+// VAR: resident PCG variant (0 pipelined, 1 Chronopoulos-Gear, 2 two
+// all-reduces). One instantiation per (PPT, VAR) keeps each kernel's code
+// and register allocation to the one PCG loop it runs.
+template <int PPT, int VAR>
 __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
   GridCtx c{a.slots, gridDim.x, a.base_tag, 0u, 0, 1u};
   const Range rg = my_range(a);
@@ -720,7 +727,7 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
     } else if (w[2] > 0.0) {
       status = DFUSE_E_CG_DIVERGENCE;
     } else {
-      status = pcg_solve<PPT>(c, a, rg, w[0], w[1], &its);
+      status = pcg_solve<PPT, VAR>(c, a, rg, w[0], w[1], &its);
       // diagnostics (DFUSE_PCG_REPEAT=n[,sweep]): solve the same system n-1
       // more times in this launch, optionally after a streaming sweep
       for (int rep = 1; rep < a.diag_repeat && status == 0; ++rep) {
@@ -729,7 +736,7 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
             a.q[i] = a.diag[i] * a.right[i] + a.down[i] * a.b[i];
           grid_sync(c);
         }
-        status = pcg_solve<PPT>(c, a, rg, w[0], w[1], &its);
+        status = pcg_solve<PPT, VAR>(c, a, rg, w[0], w[1], &its);
       }
     }
     if (leader) ctl->pcg_last = its;
@@ -742,16 +749,18 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
     const bool ls_mode = a.mode == DFUSE_MODE_LSSCALE;
     const bool depth_solvable = !ls_mode || inliers > 0;
     int cost_evals = 0, pcg_total = 0, gn_done = 0;
-    const bool otr = a.trace && leader;  // DFUSE_TRACE: cycles per GN phase, CTA 0
-    long long ot[5] = {0, 0, 0, 0, 0}, o_last = 0;
+    const bool otr = a.trace && leader;  // DFUSE_TRACE: ns per GN phase, CTA 0
+    __shared__ long long ot[6];          // [5] = last timestamp (thread 0 only)
+    if (otr)
+      for (int k = 0; k < 6; ++k) ot[k] = 0;
 #define DF_OTRACE(k)                \
   if (otr) {                        \
     const long long t_ = df_now(); \
-    ot[k] += t_ - o_last;           \
-    o_last = t_;                    \
+    ot[k] += t_ - ot[5];            \
+    ot[5] = t_;                     \
   }
     for (int it = 0; it < a.gn && status == 0; ++it) {
-      if (otr) o_last = df_now();
+      if (otr) ot[5] = df_now();
       if (!ls_mode && a.est_scale && inliers > 0) {  // fusion.hpp:411-425
         const double ln_s0 = log(scale);
         double ln_s = ln_s0;
@@ -815,7 +824,7 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
           if (v[2] > 0.0) {
             status = DFUSE_E_CG_DIVERGENCE;
           } else {
-            status = pcg_solve<PPT>(c, a, rg, v[0], v[1], &its);
+            status = pcg_solve<PPT, VAR>(c, a, rg, v[0], v[1], &its);
           }
         }
         DF_OTRACE(3);
@@ -982,10 +991,10 @@ int fusion_grid(dfuse_ctx* ctx) {
   static int occ = -1;
   if (occ < 0) {
     int o[5] = {0, 0, 0, 0, 0};
-    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[0], k_fusion<0>, FT, 0));
-    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[1], k_fusion<4>, FT, 0));
-    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[2], k_fusion<5>, FT, 0));
-    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[3], k_fusion<6>, FT, 0));
+    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[0], k_fusion<0, 0>, FT, 0));
+    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[1], k_fusion<4, 0>, FT, 0));
+    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[2], k_fusion<5, 0>, FT, 0));
+    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[3], k_fusion<6, 0>, FT, 0));
     DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[4], k_gradient, FT, 0));
     occ = o[0];
     for (int k = 1; k < 5; ++k)
@@ -1035,36 +1044,37 @@ void plan_tiles(FusionArgs& a, int grid) {
   a.th_max = (a.H + by - 1) / by;
   const long T = (long)a.tw_max * a.th_max;
   a.ppt = T <= 4L * FT ? 4 : (T <= 5L * FT ? 5 : (T <= 6L * FT ? 6 : 0));
-  if (pcg_tile_smem(a.tw_max, a.th_max) > kMaxDynSmem) a.ppt = 0;
+  if (a.ppt > 0 && pcg_tile_smem(a.ppt, a.tw_max, a.th_max) > kMaxDynSmem) a.ppt = 0;
   // LL flags are 32-bit: the whole launch must fit
   if ((double)a.gn * ((double)a.cg_max + 2.0) > 2.0e9) a.ppt = 0;
   if (!a.halo) a.ppt = 0;
 }
 
-template <int PPT>
+template <int PPT, int VAR = 0>
 static void launch_fusion_t(dfuse_ctx* ctx, FusionArgs& a, int grid) {
   size_t smem = 0;
   if (PPT > 0) {
-    smem = pcg_tile_smem(a.tw_max, a.th_max);
+    smem = pcg_tile_smem(PPT, a.tw_max, a.th_max);
     static size_t configured = 0;
     if (smem > configured) {
-      DF_CUDA(cudaFuncSetAttribute((const void*)k_fusion<PPT>,
+      DF_CUDA(cudaFuncSetAttribute((const void*)k_fusion<PPT, VAR>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       configured = smem;
     }
   }
   void* args[] = {&a};
-  DF_CUDA(cudaLaunchCooperativeKernel((const void*)k_fusion<PPT>, dim3(grid), dim3(FT), args,
+  DF_CUDA(cudaLaunchCooperativeKernel((const void*)k_fusion<PPT, VAR>, dim3(grid), dim3(FT), args,
                                       smem, ctx->stream));
 }
 
 void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
   plan_tiles(a, grid);
   if (ctx->force_streaming == 1) a.ppt = 0;
-  a.pcg_2r = ctx->force_streaming == 2;
+  a.pcg_variant = ctx->force_streaming == 2 ? 2 : (ctx->force_streaming == 3 ? 1 : 0);
+  if (a.ppt == 6 && a.pcg_variant != 0) a.ppt = 0;  // A/B variants: PPT 4 and 5 only
   {  // scale-round staging lives in the resident PCG's shared memory
     const long range = ((long)a.W * a.H + grid - 1) / grid;
-    a.stage_n = (a.ppt > 0 && (size_t)(16 * range) <= pcg_tile_smem(a.tw_max, a.th_max))
+    a.stage_n = (a.ppt > 0 && (size_t)(16 * range) <= pcg_tile_smem(a.ppt, a.tw_max, a.th_max))
                     ? (int)range
                     : 0;
   }
@@ -1082,14 +1092,17 @@ void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
     a.dbg = (long long*)scratch(ctx, S_TMP4, sizeof(long long) * dbg_n);
     DF_CUDA(cudaMemsetAsync(a.dbg, 0, sizeof(long long) * dbg_n, ctx->stream));
   }
-  if (a.ppt == 4)
-    launch_fusion_t<4>(ctx, a, grid);
-  else if (a.ppt == 5)
-    launch_fusion_t<5>(ctx, a, grid);
-  else if (a.ppt == 6)
-    launch_fusion_t<6>(ctx, a, grid);
-  else
-    launch_fusion_t<0>(ctx, a, grid);
+  const int key = a.ppt * 10 + a.pcg_variant;
+  switch (key) {
+    case 40: launch_fusion_t<4, 0>(ctx, a, grid); break;
+    case 41: launch_fusion_t<4, 1>(ctx, a, grid); break;
+    case 42: launch_fusion_t<4, 2>(ctx, a, grid); break;
+    case 50: launch_fusion_t<5, 0>(ctx, a, grid); break;
+    case 51: launch_fusion_t<5, 1>(ctx, a, grid); break;
+    case 52: launch_fusion_t<5, 2>(ctx, a, grid); break;
+    case 60: launch_fusion_t<6, 0>(ctx, a, grid); break;
+    default: launch_fusion_t<0, 0>(ctx, a, grid); break;
+  }
   DF_LAUNCHED(ctx);
   if (ctx->trace) {  // diagnostics only (DFUSE_TRACE=1): per-phase cycles of the resident PCG
     long long tr[16];

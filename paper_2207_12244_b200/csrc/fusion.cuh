@@ -63,7 +63,7 @@ struct FusionArgs {
   unsigned long long* halo;     // resident PCG LL halo words [3][P][2], or null
   int tiles_x, tiles_y, tw_max, th_max, ppt;  // resident-PCG tiling (set by launch_fusion)
   int diag_repeat, diag_sweep;  // OP_PCG diagnostics (DFUSE_PCG_REPEAT)
-  int pcg_2r;  // resident PCG with two all-reduces per iteration (A/B partner)
+  int pcg_variant;  // resident PCG: 0 pipelined (default), 1 Chronopoulos-Gear, 2 two all-reduces
   int trace;  // record per-phase cycle counts of the resident PCG in ctl->trace
   int stage_n;  // > 0: scale rounds 1-2 read round 0's values from shared memory
   long long* dbg;  // DFUSE_TRACE=2: per-CTA phase times [grid][8]

@@ -4,7 +4,18 @@
 // (fusion.hpp:316-368), up to algebraic rearrangements that change rounding
 // at the ulp level only (tolerance parity):
 //
-//   pcg_resident     (default) one grid all-reduce per iteration. The
+//   pcg_resident_pipe (default) pipelined PCG (Ghysels & Vanroose 2014,
+//                    "Hiding global synchronization latency in the
+//                    preconditioned Conjugate Gradient algorithm", Alg. 3,
+//                    with the Jacobi preconditioner applied directly:
+//                    u = r/diag, m = w/diag). Besides r it carries
+//                        w = H u,  s = H p,  z = H M^-1 s
+//                    by recurrence, so the iteration's one all-reduce of
+//                    (r.u, w.u, r.r) is posted right after the vector update
+//                    and travels while the CTA exchanges the halo of
+//                    m = M^-1 w and runs the SpMV n = H m. The curvature is
+//                    p.q = w.u - beta (r.u) / alpha_prev as below.
+//   pcg_resident     one grid all-reduce per iteration. The
 //                    direction product q = H p is carried by the recurrence
 //                        p_k = z_k + beta_k p_{k-1},  q_k = H z_k + beta_k q_{k-1}
 //                    and the curvature p_k.q_k by the Chronopoulos-Gear identity
@@ -12,6 +23,7 @@
 //                    (exact for a symmetric H with M^-1-orthogonal residuals),
 //                    so (r.r, r.z, z.Hz) travel in ONE all-reduce that follows
 //                    the SpMV.
+//                    (dfuse_ctx_set_solver_path(ctx, 3)).
 //   pcg_resident_2r  two all-reduces per iteration: (p.q) as the reference
 //                    computes it, and a split-phase (r.r, r.z) that overlaps
 //                    the next SpMV. Kept as the A/B partner
@@ -38,71 +50,111 @@
 template <int PPT>
 struct PcgTile {
   TileGeo tg;
-  int T, pw, ring_n;
-  double *s_diag, *s_rdiag, *s_right, *s_left, *s_down, *s_up, *s_z, *s_x;
-  int so_[PPT];  // offset in s_z
-  int gi_[PPT];  // global pixel index (-1: no pixel); bit 30 set: tile boundary
+  int T, pw;
+  // shared memory: eight per-pixel planes of PPT*FT doubles at fixed offsets
+  // (so every access is one base register plus an immediate), then z/m with
+  // its one-pixel halo
+  static constexpr int TMX = PPT * FT;
+  __device__ __forceinline__ static double* sm() {
+    extern __shared__ double dsm[];
+    return dsm;
+  }
+  __device__ __forceinline__ double* s_diag() const { return sm(); }
+  __device__ __forceinline__ double* s_rdiag() const { return sm() + TMX; }
+  __device__ __forceinline__ double* s_right() const { return sm() + 2 * TMX; }
+  __device__ __forceinline__ double* s_left() const { return sm() + 3 * TMX; }
+  __device__ __forceinline__ double* s_down() const { return sm() + 4 * TMX; }
+  __device__ __forceinline__ double* s_up() const { return sm() + 5 * TMX; }
+  __device__ __forceinline__ double* s_x() const { return sm() + 6 * TMX; }
+  __device__ __forceinline__ double* s_p() const { return sm() + 7 * TMX; }
+  __device__ __forceinline__ double* s_z() const { return sm() + 8 * TMX; }
+  // per pixel slot j (local index k = threadIdx.x + FT j) one int: the
+  // tile row ly, bit 30 = tile boundary, -1 = no pixel. The global index
+  // g0 + k + ly (W - tw) and the halo-plane offset k + 2 ly + tw + 3 follow
+  // from it, so the slot map costs PPT + 2 registers.
+  int lyb_[PPT];
+  int g0, wmt;  // y0 W + x0, W - tw
 
-  __device__ __forceinline__ int gi(int j) const { return gi_[j] & ~(1 << 30); }
-  __device__ __forceinline__ bool boundary(int j) const { return gi_[j] & (1 << 30); }
+  __device__ __forceinline__ bool valid(int j) const { return lyb_[j] >= 0; }
+  __device__ __forceinline__ bool boundary(int j) const { return lyb_[j] & (1 << 30); }
+  __device__ __forceinline__ int ly(int j) const { return lyb_[j] & ((1 << 30) - 1); }
+  __device__ __forceinline__ int gi(int j) const {
+    return g0 + (int)threadIdx.x + FT * j + ly(j) * wmt;
+  }
+  __device__ __forceinline__ int so(int j) const {
+    return (int)threadIdx.x + FT * j + 2 * ly(j) + tg.tw + 3;
+  }
 
   // load the tile's couplings, r, and z = r/diag; post boundary z with `flag`
-  __device__ __forceinline__ void load(const FusionArgs& a, double (&rr_)[PPT], double (&zr)[PPT],
-                                       unsigned long long* z_ll, unsigned flag) {
-    extern __shared__ double dsm[];
+  // tile geometry and this thread's pixel map (no memory traffic)
+  __device__ __forceinline__ void map(const FusionArgs& a) {
     tg = my_tile(a);
     T = tg.tw * tg.th;
-    const int TM = a.tw_max * a.th_max;
-    s_diag = dsm;
-    s_rdiag = dsm + TM;
-    s_right = dsm + 2 * TM;
-    s_left = dsm + 3 * TM;
-    s_down = dsm + 4 * TM;
-    s_up = dsm + 5 * TM;
-    s_z = dsm + 6 * TM;  // (th+2) x (tw+2), halo included
-    s_x = s_z + (a.th_max + 2) * (a.tw_max + 2);
     pw = tg.tw + 2;
-    ring_n = T > 0 ? 2 * (tg.tw + tg.th) : 0;
+
+    g0 = tg.y0 * a.W + tg.x0;
+    wmt = a.W - tg.tw;
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      const int k = threadIdx.x + FT * j;
+      lyb_[j] = -1;
+      if (k < T) {
+        const int ly = k / tg.tw, lx = k - ly * tg.tw;
+        const bool bd = lx == 0 || ly == 0 || lx == tg.tw - 1 || ly == tg.th - 1;
+        lyb_[j] = ly | (bd ? (1 << 30) : 0);
+      }
+    }
+  }
+
+  __device__ __forceinline__ void load(const FusionArgs& a, double (&rr_)[PPT], double (&zr)[PPT],
+                                       unsigned long long* z_ll, unsigned flag) {
+    tg = my_tile(a);
+    T = tg.tw * tg.th;
+    pw = tg.tw + 2;
+
     const int W = a.W, H = a.H;
+    g0 = tg.y0 * W + tg.x0;
+    wmt = W - tg.tw;
     // halo entries outside the image stay 0 (their couplings are 0 too)
-    for (int t = threadIdx.x; t < (tg.th + 2) * pw; t += FT) s_z[t] = 0.0;
+    for (int t = threadIdx.x; t < (tg.th + 2) * pw; t += FT) s_z()[t] = 0.0;
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
       const int k = threadIdx.x + FT * j;
       rr_[j] = zr[j] = 0.0;
-      gi_[j] = -1;
-      so_[j] = 0;
+      lyb_[j] = -1;
       if (k < T) {
-        s_x[k] = 0.0;
+        s_x()[k] = 0.0;
+        s_p()[k] = 0.0;
         const int ly = k / tg.tw, lx = k - ly * tg.tw;
         const int gx = tg.x0 + lx, gy = tg.y0 + ly;
         const int g = gy * W + gx;
         const bool bd = lx == 0 || ly == 0 || lx == tg.tw - 1 || ly == tg.th - 1;
-        gi_[j] = g | (bd ? (1 << 30) : 0);
-        so_[j] = (ly + 1) * pw + lx + 1;
+        lyb_[j] = ly | (bd ? (1 << 30) : 0);
         const double d = __ldcg(a.diag + g);
         const double rd = 1.0 / d;
-        s_diag[k] = d;
-        s_rdiag[k] = rd;
-        s_right[k] = gx + 1 < W ? __ldcg(a.right + g) : 0.0;
-        s_left[k] = gx > 0 ? __ldcg(a.right + g - 1) : 0.0;
-        s_down[k] = gy + 1 < H ? __ldcg(a.down + g) : 0.0;
-        s_up[k] = gy > 0 ? __ldcg(a.down + g - W) : 0.0;
+        s_diag()[k] = d;
+        s_rdiag()[k] = rd;
+        s_right()[k] = gx + 1 < W ? __ldcg(a.right + g) : 0.0;
+        s_left()[k] = gx > 0 ? __ldcg(a.right + g - 1) : 0.0;
+        s_down()[k] = gy + 1 < H ? __ldcg(a.down + g) : 0.0;
+        s_up()[k] = gy > 0 ? __ldcg(a.down + g - W) : 0.0;
         const double r = __ldcg(a.r + g);
         rr_[j] = r;
         const double q0 = r * rd;  // z = r/diag, fusion.hpp:329
         const double z = __fma_rn(__fma_rn(-q0, d, r), rd, q0);
         zr[j] = z;
-        s_z[so_[j]] = z;
+        s_z()[so(j)] = z;
         if (bd) ll_store(z_ll + 2 * (long)g, z, flag);
       }
     }
   }
 
-  // halo ring of z (version `flag`) from the neighbours' LL words
+  // halo ring of z (version `flag`) from the neighbours' LL words: one
+  // thread per ring cell, all loads in flight at once
   __device__ __forceinline__ void ring(const FusionArgs& a, const unsigned long long* z_ll,
                                        unsigned flag) const {
+    const int ring_n = T > 0 ? 2 * (tg.tw + tg.th) : 0;
     for (int t = threadIdx.x; t < ring_n; t += FT) {
       int gx, gy, so;
       if (t < tg.tw) {
@@ -116,7 +168,7 @@ struct PcgTile {
         so = (t - 2 * tg.tw - tg.th + 1) * pw + tg.tw + 1;
       }
       if (gx >= 0 && gx < a.W && gy >= 0 && gy < a.H)
-        s_z[so] = ll_wait(z_ll + 2 * ((long)gy * a.W + gx), flag);
+        s_z()[so] = ll_wait(z_ll + 2 * ((long)gy * a.W + gx), flag);
     }
   }
 
@@ -127,15 +179,15 @@ struct PcgTile {
   __device__ __forceinline__ void spmv(const double (&zr)[PPT], double (&wv)[PPT]) const {
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      if (gi_[j] >= 0 && boundary(j) == BOUNDARY) {
-        const int k = threadIdx.x + FT * j, so = so_[j];
-        double v = s_diag[k] * zr[j];
-        v += s_right[k] * s_z[so + 1];
-        v += s_left[k] * s_z[so - 1];
-        v += s_down[k] * s_z[so + pw];
-        v += s_up[k] * s_z[so - pw];
+      if (valid(j) && boundary(j) == BOUNDARY) {
+        const int k = threadIdx.x + FT * j, so = this->so(j);
+        double v = s_diag()[k] * zr[j];
+        v += s_right()[k] * s_z()[so + 1];
+        v += s_left()[k] * s_z()[so - 1];
+        v += s_down()[k] * s_z()[so + pw];
+        v += s_up()[k] * s_z()[so - pw];
         wv[j] = v;
-      } else if (gi_[j] < 0) {
+      } else if (!valid(j)) {
         wv[j] = 0.0;
       }
     }
@@ -145,61 +197,75 @@ struct PcgTile {
   __device__ __forceinline__ void store_x(const FusionArgs& a) const {
 #pragma unroll
     for (int j = 0; j < PPT; ++j)
-      if (gi_[j] >= 0) a.x[gi(j)] = s_x[threadIdx.x + FT * j];
+      if (valid(j)) a.x[gi(j)] = s_x()[threadIdx.x + FT * j];
   }
 };
 
 // DFUSE_TRACE: thread 0 accumulates SM cycles per phase (CTA 0 -> ctl->trace,
 // every CTA -> a.dbg[cta][phase] when DFUSE_TRACE=2); the host converts
 // cycles to ns with the clock measured over the whole solve
+// The accumulators live in shared memory (only thread 0 touches them), so
+// the instrumentation costs the solver loop one predicate register.
 struct PcgTrace {
   bool on;
-  long long tr[6], t_last, t_start, c_start;
-  __device__ __forceinline__ explicit PcgTrace(const FusionArgs& a)
+  __device__ __forceinline__ static long long* st() {
+    __shared__ long long s[9];  // tr[6], t_last, t_start, c_start
+    return s;
+  }
+  __device__ __forceinline__ explicit PcgTrace(const FusionArgs& a, bool resume = false)
       : on(a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || a.trace == 2)) {
-    for (int k = 0; k < 6; ++k) tr[k] = 0;
-    t_start = on ? df_now() : 0;
-    t_last = c_start = on ? clock64() : 0;
+    if (on && !resume) {
+      long long* s = st();
+      for (int k = 0; k < 6; ++k) s[k] = 0;
+      s[7] = df_now();
+      s[6] = s[8] = clock64();
+    }
   }
   __device__ __forceinline__ void mark(int k) {
     if (on) {
+      long long* s = st();
       const long long t = clock64();
-      tr[k] += t - t_last;
-      t_last = t;
+      s[k] += t - s[6];
+      s[6] = t;
     }
   }
   __device__ __forceinline__ void flush(const FusionArgs& a) {
-    if (on && blockIdx.x == 0) {
-      for (int k = 0; k < 6; ++k) a.ctl->trace[k] += tr[k];
-      a.ctl->trace[6] += df_now() - t_start;   // ns
-      a.ctl->trace[7] += clock64() - c_start;  // SM cycles -> effective clock
+    if (!on) return;
+    const long long* s = st();
+    if (blockIdx.x == 0) {
+      for (int k = 0; k < 6; ++k) a.ctl->trace[k] += s[k];
+      a.ctl->trace[6] += df_now() - s[7];   // ns
+      a.ctl->trace[7] += clock64() - s[8];  // SM cycles -> effective clock
     }
-    if (on && a.trace == 2)
-      for (int k = 0; k < 6; ++k) a.dbg[blockIdx.x * 8 + k] += tr[k];
+    if (a.trace == 2)
+      for (int k = 0; k < 6; ++k) a.dbg[blockIdx.x * 8 + k] += s[k];
   }
 };
 
-// One all-reduce per iteration (Chronopoulos-Gear). Trace phases:
-// 0 halo ring, 1 SpMV, 2 all-reduce, 5 update sweep.
+// Chronopoulos-Gear loop from iteration it0 (0: a fresh solve; > 0: resumed
+// from the pipelined variant). On entry s_z holds z (the version after it0
+// updates, boundary posted to z_ll with flag base + it0 + 1), pr/qr hold p
+// and q = H p of iteration it0-1, and (rz, alpha) are those of it0-1.
 template <int PPT>
-__device__ int pcg_resident(GridCtx& c, const FusionArgs& a, double bnorm2, double rz, int* its) {
-  PcgTile<PPT> t;
-  unsigned long long* z_ll = a.halo;  // [P][2]
-  // LL flags of this solve: z after v updates -> base + v + 1
-  const unsigned base = c.ll_next;
-  c.ll_next += (unsigned)a.cg_max + 2u;
-  double rr_[PPT], zr[PPT], pr[PPT], qr[PPT];
-  t.load(a, rr_, zr, z_ll, base + 1);
-#pragma unroll
-  for (int j = 0; j < PPT; ++j) pr[j] = qr[j] = 0.0;
-
+__device__ __forceinline__ int pcg_cg_core(GridCtx& c, const FusionArgs& a, PcgTile<PPT>& t,
+                                           PcgTrace& trc, unsigned long long* z_ll,
+                                           unsigned base, double (&rr_)[PPT], double (&zr)[PPT],
+                                           double (&pr)[PPT], double (&qr)[PPT], double bnorm2,
+                                           double rz, int it0, double alpha, double prev,
+                                           int streak, int* its) {
   const double tol2 = a.cg_tol * a.cg_tol * bnorm2;
-  double prev = bnorm2, beta = 0.0, alpha = 1.0;
+  double beta = 0.0;
   double rr_part = 0.0, rz_part = 0.0;
-  int streak = 0, status = 0;
-  *its = 0;
-  PcgTrace trc(a);
-  for (int it = 0; a.cg_max > 0; ++it) {
+  if (it0 > 0) {  // partials of the entry residual (same order as the sweep below)
+#pragma unroll
+    for (int j = 0; j < PPT; ++j)
+      if (t.valid(j)) {
+        rr_part += rr_[j] * rr_[j];
+        rz_part += rr_[j] * zr[j];
+      }
+  }
+  int status = 0;
+  for (int it = it0; a.cg_max > 0; ++it) {
     // z is the version after `it` updates; w = H z
     const bool more = it < a.cg_max;
     double wv[PPT];
@@ -258,30 +324,262 @@ __device__ int pcg_resident(GridCtx& c, const FusionArgs& a, double bnorm2, doub
     rz_part = 0.0;
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      if (t.gi_[j] >= 0) {
+      if (t.valid(j)) {
         const int k = threadIdx.x + FT * j;
         const double p = it == 0 ? zr[j] : zr[j] + beta * pr[j];
         const double q = it == 0 ? wv[j] : wv[j] + beta * qr[j];
         pr[j] = p;
         qr[j] = q;
-        t.s_x[k] = t.s_x[k] + alpha * p;
+        t.s_x()[k] = t.s_x()[k] + alpha * p;
         const double r = rr_[j] - alpha * q;
         rr_[j] = r;
         rr_part += r * r;
-        const double rd = t.s_rdiag[k];
+        const double rd = t.s_rdiag()[k];
         const double q0 = r * rd;
-        const double z = __fma_rn(__fma_rn(-q0, t.s_diag[k], r), rd, q0);
+        const double z = __fma_rn(__fma_rn(-q0, t.s_diag()[k], r), rd, q0);
         zr[j] = z;
-        t.s_z[t.so_[j]] = z;
+        t.s_z()[t.so(j)] = z;
         rz_part += r * z;
         if (t.boundary(j)) ll_store(z_ll + 2 * (long)t.gi(j), z, base + (unsigned)it + 2u);
       }
     }
     trc.mark(5);
   }
+  return status;
+}
+
+// One all-reduce per iteration (Chronopoulos-Gear). Trace phases:
+// 0 halo ring, 1 SpMV, 2 all-reduce, 5 update sweep.
+template <int PPT>
+__device__ int pcg_resident(GridCtx& c, const FusionArgs& a, double bnorm2, double rz, int* its) {
+  PcgTile<PPT> t;
+  unsigned long long* z_ll = a.halo;  // [P][2]
+  // LL flags of this solve: z after v updates -> base + v + 1
+  const unsigned base = c.ll_next;
+  c.ll_next += (unsigned)a.cg_max + 2u;
+  double rr_[PPT], zr[PPT], pr[PPT], qr[PPT];
+  t.load(a, rr_, zr, z_ll, base + 1);
+#pragma unroll
+  for (int j = 0; j < PPT; ++j) pr[j] = qr[j] = 0.0;
+  *its = 0;
+  PcgTrace trc(a);
+  const int status = pcg_cg_core<PPT>(c, a, t, trc, z_ll, base, rr_, zr, pr, qr, bnorm2, rz, 0,
+                                      1.0, bnorm2, 0, its);
   trc.flush(a);
   t.store_x(a);
   grid_sync(c);  // fenced: the trial sweeps read x at the neighbours
+  return status;
+}
+
+// relative residual r.r / b.b below which the pipelined solve hands over to
+// Chronopoulos-Gear (residual norm 1e-10 of |b|, far below cg_tol = 1e-6)
+constexpr double kPipeSwitch = 1e-20;
+
+// Pipelined: one all-reduce per iteration, in flight during the halo
+// exchange and SpMV. Trace phases: 0 halo ring, 1 SpMV, 2 all-reduce wait,
+// 5 update sweep + publish.
+//
+// The halo words of m alternate between two LL arrays by version parity: a
+// CTA posts m_{i+1} only after the all-reduce of iteration i, which needs
+// every CTA's post-update publish of iteration i-1, which each CTA makes
+// after its threads read the m_{i-1} halo. So a version is never overwritten before
+// its readers are done with it.
+struct PcgHandover {
+  int it, streak;
+  double rz, alpha, prev;
+};
+
+// returns the status, or -1 after a handover (*hand filled; x, p in shared
+// memory, the PcgTrace accumulators still open)
+template <int PPT>
+__device__ int pcg_resident_pipe(GridCtx& c, const FusionArgs& a, double bnorm2, double rz,
+                                 int* its, PcgHandover* hand) {
+  PcgTile<PPT> t;
+  const long P = (long)a.W * a.H;
+  // LL array v: a.halo + v 2P (v = 0, 1; arithmetic, not an indexed local array)
+  unsigned long long* const hb0 = a.halo;
+  // LL flags: u0 -> base + 1 (array 0); m_i -> base + i + 2 (array (i+1)&1)
+  const unsigned base = c.ll_next;
+  c.ll_next += (unsigned)a.cg_max + 3u;
+  double rr_[PPT], mr[PPT], wr[PPT], zr[PPT], sr[PPT];
+  t.load(a, rr_, mr, hb0, base + 1);  // mr = u0 = r0/diag, in s_z with halo
+  PcgTrace trc(a);
+  // w0 = H u0
+  __syncthreads();
+  t.template spmv<false>(mr, wr);
+  t.ring(a, hb0, base + 1);
+  __syncthreads();
+  t.template spmv<true>(mr, wr);
+  __syncthreads();  // every thread is done reading u0 from s_z
+  double wu = 0.0;
+#pragma unroll
+  for (int j = 0; j < PPT; ++j) {
+    zr[j] = sr[j] = 0.0;
+    if (t.valid(j)) {
+      const int k = threadIdx.x + FT * j;
+      wu += wr[j] * mr[j];  // (w0, u0)
+      const double m = wr[j] * t.s_rdiag()[k];  // m0 = w0/diag
+      mr[j] = m;
+      t.s_z()[t.so(j)] = m;
+      if (t.boundary(j)) ll_store(hb0 + 2 * P + 2 * (long)t.gi(j), m, base + 2u);
+    }
+  }
+  {
+    double v[3] = {0.0, wu, 0.0};
+    grid_allreduce_publish(c, v);
+  }
+  trc.mark(5);
+
+  const double tol2 = a.cg_tol * a.cg_tol * bnorm2;
+  double prev = bnorm2, alpha = 1.0, gamma_prev = rz;
+  int streak = 0, status = 0;
+  *its = 0;
+  for (int it = 0;; ++it) {
+    // s_z holds m_it (halo from array (it+1)&1, flag base+it+2); mr := H m_it
+    const bool more = it < a.cg_max;
+    if (more) {
+      // no barrier before the interior SpMV: the one in the last publish
+      // (cta_partial) follows every thread's s_z writes of the update sweep
+      t.template spmv<false>(mr, mr);
+      trc.mark(1);
+      t.ring(a, hb0 + (long)((it + 1) & 1) * 2 * P, base + (unsigned)it + 2u);
+      __syncthreads();
+      trc.mark(0);
+      t.template spmv<true>(mr, mr);
+      trc.mark(1);
+    }
+    double v[3];  // (r.u, w.u, r.r) of the vectors after `it` updates
+    grid_allreduce_wait(c, v);
+    trc.mark(2);
+    double gamma, beta, pq;
+    if (it == 0) {
+      gamma = rz;  // (r0, z0) as the assembly sweep computed it
+      beta = 0.0;
+      pq = v[1];
+    } else {
+      if (v[2] < kPipeSwitch * bnorm2) {
+        // Deep convergence: pipelined CG's recursive residual stagnates
+        // near eps*cond (its auxiliary recurrences drift), while the
+        // reference's keeps falling; hand the solve over to
+        // Chronopoulos-Gear (pcg_resume_cg), which re-derives this
+        // iteration's (r.r, r.z) and applies the stop rules to them. The
+        // state leaves the loop through memory (r, q = s in the r/q
+        // rasters; p, x stay in shared memory) so that the handover adds no
+        // registers to this loop.
+#pragma unroll
+        for (int j = 0; j < PPT; ++j)
+          if (t.valid(j)) {
+            a.r[t.gi(j)] = rr_[j];
+            a.q[t.gi(j)] = sr[j];
+          }
+        hand->it = it;
+        hand->rz = gamma_prev;
+        hand->alpha = alpha;
+        hand->prev = prev;
+        hand->streak = streak;
+        return -1;
+      }
+      // finish iteration it-1: fusion.hpp:350-364
+      const double rn = v[2];
+      if (rn <= tol2) break;
+      if (rn > prev) {
+        if (++streak >= 10) {
+          status = DFUSE_E_CG_DIVERGENCE;
+          break;
+        }
+      } else {
+        streak = 0;
+      }
+      prev = rn;
+      if (!more) break;
+      gamma = v[0];
+      beta = gamma / gamma_prev;
+      pq = v[1] - beta * gamma / alpha;
+    }
+    if (!(pq > 0.0)) {  // fusion.hpp:342
+      status = DFUSE_E_CG_DIVERGENCE;
+      break;
+    }
+    alpha = gamma / pq;
+    gamma_prev = gamma;
+    *its = it + 1;
+    // z = n + beta z, s = w + beta s, p = u + beta p; x += alpha p,
+    // r -= alpha s, w -= alpha z; u = r/diag, m = w/diag (fusion.hpp:345-364)
+    double ru = 0.0, wu2 = 0.0, rr = 0.0;
+    unsigned long long* hm = hb0 + (long)(it & 1) * 2 * P;  // m_{it+1}: array (it+2)&1
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      if (t.valid(j)) {
+        const int k = threadIdx.x + FT * j;
+        const double d = t.s_diag()[k], rd = t.s_rdiag()[k];
+        const double r0 = rr_[j];
+        const double uq = r0 * rd;
+        const double u = __fma_rn(__fma_rn(-uq, d, r0), rd, uq);
+        const double z = mr[j] + beta * zr[j];
+        const double sv = wr[j] + beta * sr[j];
+        const double p = u + beta * t.s_p()[k];
+        zr[j] = z;
+        sr[j] = sv;
+        t.s_p()[k] = p;
+        t.s_x()[k] = t.s_x()[k] + alpha * p;
+        const double r = r0 - alpha * sv;
+        rr_[j] = r;
+        const double w = wr[j] - alpha * z;
+        wr[j] = w;
+        const double q1 = r * rd;
+        const double un = __fma_rn(__fma_rn(-q1, d, r), rd, q1);
+        const double m = w * rd;  // M^-1 w: internal to the pipelined recurrences
+        mr[j] = m;
+        t.s_z()[t.so(j)] = m;
+        ru += r * un;
+        wu2 += w * un;
+        rr += r * r;
+        if (t.boundary(j)) ll_store(hm + 2 * (long)t.gi(j), m, base + (unsigned)it + 3u);
+      }
+    }
+    double v2[3] = {ru, wu2, rr};
+    grid_allreduce_publish(c, v2);
+    trc.mark(5);
+  }
+  trc.flush(a);
+  t.store_x(a);
+  grid_sync(c);  // fenced: the trial sweeps read x at the neighbours
+  return status;
+}
+
+// Chronopoulos-Gear continuation of a pipelined solve after its handover
+template <int PPT>
+__device__ int pcg_resume_cg(GridCtx& c, const FusionArgs& a, double bnorm2,
+                             const PcgHandover& h, int* its) {
+  PcgTile<PPT> t;
+  t.map(a);
+  PcgTrace trc(a, true);
+  const long P = (long)a.W * a.H;
+  unsigned long long* z3 = a.halo + 4 * P;  // third LL array (the pipelined solve used two)
+  const unsigned base = c.ll_next;
+  c.ll_next += (unsigned)a.cg_max + 2u;
+  double rr_[PPT], zr[PPT], pr[PPT], qr[PPT];
+#pragma unroll
+  for (int j = 0; j < PPT; ++j) {
+    rr_[j] = zr[j] = pr[j] = qr[j] = 0.0;
+    if (t.valid(j)) {
+      const int k = threadIdx.x + FT * j;
+      const double r = a.r[t.gi(j)], d = t.s_diag()[k], rd = t.s_rdiag()[k];
+      const double uq = r * rd;
+      const double u = __fma_rn(__fma_rn(-uq, d, r), rd, uq);
+      rr_[j] = r;
+      zr[j] = u;
+      pr[j] = t.s_p()[k];
+      qr[j] = a.q[t.gi(j)];
+      t.s_z()[t.so(j)] = u;
+      if (t.boundary(j)) ll_store(z3 + 2 * (long)t.gi(j), u, base + (unsigned)h.it + 1u);
+    }
+  }
+  const int status = pcg_cg_core<PPT>(c, a, t, trc, z3, base, rr_, zr, pr, qr, bnorm2, h.rz, h.it,
+                                      h.alpha, h.prev, h.streak, its);
+  trc.flush(a);
+  t.store_x(a);
+  grid_sync(c);
   return status;
 }
 
@@ -343,7 +641,7 @@ __device__ int pcg_resident_2r(GridCtx& c, const FusionArgs& a, double bnorm2, d
     double pq = 0.0;
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      if (t.gi_[j] >= 0) {
+      if (t.valid(j)) {
         const double p = it == 0 ? zr[j] : zr[j] + beta * pr[j];
         const double q = it == 0 ? wv[j] : wv[j] + beta * qr[j];
         pr[j] = p;
@@ -363,17 +661,17 @@ __device__ int pcg_resident_2r(GridCtx& c, const FusionArgs& a, double bnorm2, d
     double rr = 0.0, rzn = 0.0;
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      if (t.gi_[j] >= 0) {
+      if (t.valid(j)) {
         const int k = threadIdx.x + FT * j;
-        t.s_x[k] = t.s_x[k] + alpha * pr[j];
+        t.s_x()[k] = t.s_x()[k] + alpha * pr[j];
         const double r = rr_[j] - alpha * qr[j];
         rr_[j] = r;
         rr += r * r;
-        const double rd = t.s_rdiag[k];
+        const double rd = t.s_rdiag()[k];
         const double q0 = r * rd;
-        const double z = __fma_rn(__fma_rn(-q0, t.s_diag[k], r), rd, q0);
+        const double z = __fma_rn(__fma_rn(-q0, t.s_diag()[k], r), rd, q0);
         zr[j] = z;
-        t.s_z[t.so_[j]] = z;
+        t.s_z()[t.so(j)] = z;
         rzn += r * z;
         if (t.boundary(j)) ll_store(z_ll + 2 * (long)t.gi(j), z, base + (unsigned)it + 2u);
       }
@@ -393,7 +691,7 @@ __device__ int pcg_resident_2r(GridCtx& c, const FusionArgs& a, double bnorm2, d
   return status;
 }
 
-// shared memory of the resident PCG for a tw_max x th_max tile
-inline size_t pcg_tile_smem(int tw_max, int th_max) {
-  return sizeof(double) * (7 * (size_t)tw_max * th_max + (size_t)(th_max + 2) * (tw_max + 2));
+// shared memory of the resident PCG for a tw_max x th_max tile at ppt pixels per thread
+inline size_t pcg_tile_smem(int ppt, int tw_max, int th_max) {
+  return sizeof(double) * (8 * (size_t)ppt * FT + (size_t)(th_max + 2) * (tw_max + 2));
 }
