@@ -118,7 +118,8 @@ struct FusionWS {
   double* sv;
   uint8_t* svalid;
   double* lnsd;
-  double* semR;
+  double* irs;
+  double* ivar[3];
   double* ld[2];
   double *diag, *right, *down, *b, *x, *r, *p0, *p1, *q;
   ReduceSlot* slots;
@@ -132,7 +133,7 @@ size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 FusionWS alloc_fusion_ws(dfuse_ctx* ctx, long P, int grid, int slot) {
   const size_t dP = align_up(sizeof(double) * P);
   const bool resident = fusion_resident_possible(P, grid);
-  size_t total = 6 * dP + 4 * dP + align_up(P) + 11 * dP + align_up(fusion_slots_bytes(grid)) +
+  size_t total = 6 * dP + 7 * dP + align_up(P) + 11 * dP + align_up(fusion_slots_bytes(grid)) +
                  align_up(sizeof(FusionControl)) + align_up(2 * sizeof(FusionStateDev)) +
                  (resident ? align_up(fusion_halo_bytes(P)) : 0);
   char* base = (char*)scratch(ctx, slot, total);
@@ -148,7 +149,8 @@ FusionWS alloc_fusion_ws(dfuse_ctx* ctx, long P, int grid, int slot) {
   w.sv = (double*)take(dP);
   w.svalid = (uint8_t*)take(P);
   w.lnsd = (double*)take(dP);
-  w.semR = (double*)take(dP);
+  w.irs = (double*)take(dP);
+  for (int k = 0; k < 3; ++k) w.ivar[k] = (double*)take(dP);
   w.ld[0] = (double*)take(dP);
   w.ld[1] = (double*)take(dP);
   w.diag = (double*)take(dP);
@@ -177,7 +179,8 @@ void fill_args(FusionArgs& a, const FusionWS& w, int W, int H) {
   a.sv = w.sv;
   a.svalid = w.svalid;
   a.lnsd = w.lnsd;
-  a.semR = w.semR;
+  a.irs = w.irs;
+  for (int k = 0; k < 3; ++k) a.ivar[k] = w.ivar[k];
   a.ld[0] = w.ld[0];
   a.ld[1] = w.ld[1];
   a.diag = w.diag;

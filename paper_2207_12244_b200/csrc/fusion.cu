@@ -345,25 +345,29 @@ __device__ void grid_allreduce_wait(GridCtx& c, double (&v)[NV]) {
 // ---------------------------------------------------------------------------
 // per-pixel terms (gather form)
 struct PlainLd {
+  static constexpr bool kTrial = false;
   const double* ld;
   __device__ __forceinline__ double operator()(int j) const { return ld[j]; }
 };
 struct TrialLd {  // trial.log_depth = st + step * delta, fusion.hpp:432-433
+  static constexpr bool kTrial = true;
   const double* ld;
   const double* x;
   double step;
   __device__ __forceinline__ double operator()(int j) const { return ld[j] + step * x[j]; }
 };
 
-// total_cost's contribution of pixel i, fusion.hpp:234-250 (terms added in
-// the reference's order into a per-pixel sum)
+// total_cost's contribution of pixel i with the reference's own arithmetic
+// (fusion.hpp:234-250; divisions by the variances). Used by k_gradient, the
+// test-only cost_gradient kernel.
 template <class LD>
-__device__ __forceinline__ double pixel_cost(const FusionArgs& a, const Sel& sel, int i, int x,
-                                             int y, const LD& L, double li, double ln_s) {
+__device__ __forceinline__ double pixel_cost_exact(const FusionArgs& a, const Sel& sel, int i,
+                                                   int x, int y, const LD& L, double li,
+                                                   double ln_s) {
   double c = 0.0;
   if (sel.net) c += huber_c(li - a.pred[0][i], a.dnet) / a.pred[1][i];
   if (a.svalid[i])
-    c += huber_c(li - ln_s - a.lnsd[i], a.dsemi) / a.semR[i];
+    c += huber_c(li - ln_s - log(a.sd[i]), a.dsemi) / semi_logvar(a.sv[i], a.sd[i]);
   if (sel.grad && x + 1 < a.W) c += huber_c(L(i + 1) - li - a.pred[2][i], a.dgrad) / a.pred[3][i];
   if (sel.grad && y + 1 < a.H)
     c += huber_c(L(i + a.W) - li - a.pred[4][i], a.dgrad) / a.pred[5][i];
@@ -384,44 +388,158 @@ __device__ __forceinline__ Range my_range(const FusionArgs& a) {
 
 // ---------------------------------------------------------------------------
 // sweeps (every sweep walks the CTA's range with the same thread->pixel map,
-// so per-pixel values a thread writes are read back by that thread)
+// so per-pixel values a thread writes are read back by that thread).
+//
+// The sweeps are latency-bound gathers from L2, so they are written for
+// memory-level parallelism: each thread walks its pixels in fully unrolled,
+// predicated groups of U; every load of a pixel is unconditional (indices
+// clamped to the pixel itself where the reference skips a term) and the
+// skipped terms are removed with selects, and the arrays come in as
+// __restrict__ parameters, so the compiler can issue all of a group's loads
+// before the first result is needed (a branch per term, or a possibly
+// aliasing store, would serialise one L2 round trip per term).
+//
+// Per-call planes (sweep_prologue): ln d_semi and 1/R_semi (0 where the semi
+// map has no value) and the reciprocals of the three prediction variances.
+// Each weighted term is then huber * (1/var) where the reference computes
+// huber / var: equal up to one rounding (tolerance parity).
 
-// per-call constants of the semi term: ln d_semi and R = semi_log_variance
-// (fusion.hpp:95-100,195-196), computed once instead of in every sweep
-__device__ void sweep_semi_prologue(const FusionArgs& a, const Range& rg) {
-  for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT)
-    if (a.svalid[i]) {
-      a.lnsd[i] = log(a.sd[i]);
-      a.semR[i] = semi_logvar(a.sv[i], a.sd[i]);
+struct SweepPlanes {
+  const double* __restrict__ p0;  // pred log_depth
+  const double* __restrict__ p2;  // pred grad_x
+  const double* __restrict__ p4;  // pred grad_y
+  const double* __restrict__ iv0;  // 1 / log_depth_var
+  const double* __restrict__ iv1;  // 1 / grad_x_var
+  const double* __restrict__ iv2;  // 1 / grad_y_var
+  const uint8_t* __restrict__ sval;
+  const double* __restrict__ lns;  // ln d_semi (0 if invalid)
+  const double* __restrict__ irs;  // 1 / semi_log_variance (0 if invalid)
+};
+
+__device__ __forceinline__ SweepPlanes planes_of(const FusionArgs& a) {
+  return SweepPlanes{a.pred[0], a.pred[2], a.pred[4], a.ivar[0], a.ivar[1],
+                     a.ivar[2], a.svalid, a.lnsd, a.irs};
+}
+
+__device__ void sweep_prologue(const FusionArgs& a, const Range& rg) {
+  for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) {
+    const bool v = a.svalid[i];
+    const double d = a.sd[i];
+    a.lnsd[i] = v ? log(d) : 0.0;                          // fusion.hpp:195
+    a.irs[i] = v ? 1.0 / semi_logvar(a.sv[i], d) : 0.0;    // fusion.hpp:95-100,196
+    a.ivar[0][i] = 1.0 / a.pred[1][i];
+    a.ivar[1][i] = 1.0 / a.pred[3][i];
+    a.ivar[2][i] = 1.0 / a.pred[5][i];
+  }
+}
+
+// one pixel's total_cost terms (fusion.hpp:234-250, reference order) from
+// loaded values; lr / ldn = log-depth at i+1 / i+W (any value when absent)
+__device__ __forceinline__ double cost_terms(const Sel sel, const bool hasr, const bool hasd,
+                                             const double li, const double lr, const double ldn,
+                                             const double q0, const double i0, const bool sv,
+                                             const double ln, const double ir, const double q2,
+                                             const double i1, const double q4, const double i2,
+                                             const double dnet, const double dsemi,
+                                             const double dgrad, const double ln_s) {
+  double c = 0.0;
+  if (sel.net) c += huber_c(li - q0, dnet) * i0;
+  const double ts = huber_c(li - ln_s - ln, dsemi) * ir;
+  c += sv ? ts : 0.0;
+  if (sel.grad) {
+    const double tx = huber_c(lr - li - q2, dgrad) * i1;
+    c += hasr ? tx : 0.0;
+    const double ty = huber_c(ldn - li - q4, dgrad) * i2;
+    c += hasd ? ty : 0.0;
+  }
+  return c;
+}
+
+// total_cost of ld (+ step * xs when TRIAL); wt: also store the evaluated
+// log-depth (the trial state)
+template <int U, bool TRIAL>
+__device__ __forceinline__ double sweep_cost_body(const Range rg, const int W, const int H,
+                                                  const Sel sel, const double dnet,
+                                                  const double dsemi, const double dgrad,
+                                                  const double ln_s, const double* __restrict__ ld,
+                                                  const double* __restrict__ xs, const double step,
+                                                  const SweepPlanes pl, double* __restrict__ wt) {
+  double cost = 0.0;
+  for (int i0 = rg.beg + threadIdx.x; i0 < rg.end; i0 += U * FT) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int iu = i0 + u * FT;
+      const bool in = iu < rg.end;
+      const int i = in ? iu : rg.beg;
+      const int y = i / W, x = i - y * W;
+      const bool hasr = x + 1 < W, hasd = y + 1 < H;
+      const int ir = hasr ? i + 1 : i, id = hasd ? i + W : i;
+      const double li = TRIAL ? ld[i] + step * xs[i] : ld[i];
+      const double lr = TRIAL ? ld[ir] + step * xs[ir] : ld[ir];
+      const double ldn = TRIAL ? ld[id] + step * xs[id] : ld[id];
+      const double c = cost_terms(sel, hasr, hasd, li, lr, ldn, pl.p0[i], pl.iv0[i], pl.sval[i],
+                                  pl.lns[i], pl.irs[i], pl.p2[i], pl.iv1[i], pl.p4[i], pl.iv2[i],
+                                  dnet, dsemi, dgrad, ln_s);
+      if (in) {
+        if (wt) wt[i] = li;
+        cost += c;
+      }
     }
+  }
+  return cost;
+}
+
+template <int U, class LD>
+__device__ double sweep_cost(const FusionArgs& a, const Sel& sel, const Range& rg, const LD& L,
+                             double ln_s, double* write_trial) {
+  if constexpr (LD::kTrial)  // trial = st + step * delta (fusion.hpp:432-433)
+    return sweep_cost_body<U, true>(rg, a.W, a.H, sel, a.dnet, a.dsemi, a.dgrad, ln_s, L.ld, L.x,
+                                    L.step, planes_of(a), write_trial);
+  else
+    return sweep_cost_body<U, false>(rg, a.W, a.H, sel, a.dnet, a.dsemi, a.dgrad, ln_s, L.ld,
+                                     nullptr, 0.0, planes_of(a), write_trial);
 }
 
 // scale IRLS round (fusion.hpp:379-388) [+ total_cost at ln_s_cost]
-// stage (optional, shared memory): offset and R of the CTA's pixels for the
-// later rounds (R = -1 marks a pixel without a semi-dense value)
-__device__ void sweep_scale(const FusionArgs& a, const Sel& sel, const Range& rg,
-                            const double* ld, double ln_s, bool with_cost, double ln_s_cost,
-                            double (&v)[4], double* stage = nullptr, int stage_n = 0) {
+// stage (optional, shared memory): offset and 1/R of the CTA's pixels for the
+// later rounds (1/R = -1 marks a pixel without a semi-dense value)
+template <int U>
+__device__ __forceinline__ void sweep_scale_body(const Range rg, const int W, const int H,
+                                                 const Sel sel, const double dnet,
+                                                 const double dsemi, const double dgrad,
+                                                 const double* __restrict__ ld, const double ln_s,
+                                                 const bool with_cost, const double ln_s_cost,
+                                                 const SweepPlanes pl, double (&v)[4],
+                                                 double* __restrict__ stage, const int stage_n) {
   double num = 0.0, den = 0.0, cost = 0.0;
-  PlainLd L{ld};
-  for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) {
-    const double li = ld[i];
-    if (a.svalid[i]) {
-      const double offset = li - a.lnsd[i];
-      const double R = a.semR[i];
-      const double wi = huber_w(offset - ln_s, a.dsemi) / R;
-      num += wi * offset;
-      den += wi;
-      if (stage) {
-        stage[i - rg.beg] = offset;
-        stage[stage_n + i - rg.beg] = R;
+  for (int i0 = rg.beg + threadIdx.x; i0 < rg.end; i0 += U * FT) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int iu = i0 + u * FT;
+      const bool in = iu < rg.end;
+      const int i = in ? iu : rg.beg;
+      const double li = ld[i];
+      const bool sv = pl.sval[i];
+      const double ln = pl.lns[i], ir = pl.irs[i];
+      const double offset = li - ln;
+      const double wi = huber_w(offset - ln_s, dsemi) * ir;
+      if (in) {
+        num += sv ? wi * offset : 0.0;
+        den += sv ? wi : 0.0;
+        if (stage) {
+          stage[i - rg.beg] = offset;
+          stage[stage_n + i - rg.beg] = sv ? ir : -1.0;
+        }
       }
-    } else if (stage) {
-      stage[stage_n + i - rg.beg] = -1.0;
-    }
-    if (with_cost) {
-      const int y = i / a.W, x = i - y * a.W;
-      cost += pixel_cost(a, sel, i, x, y, L, li, ln_s_cost);
+      if (with_cost) {
+        const int y = i / W, x = i - y * W;
+        const bool hasr = x + 1 < W, hasd = y + 1 < H;
+        const double c = cost_terms(sel, hasr, hasd, li, ld[hasr ? i + 1 : i],
+                                    ld[hasd ? i + W : i], pl.p0[i], pl.iv0[i], sv, ln, ir,
+                                    pl.p2[i], pl.iv1[i], pl.p4[i], pl.iv2[i], dnet, dsemi, dgrad,
+                                    ln_s_cost);
+        if (in) cost += c;
+      }
     }
   }
   v[0] = num;
@@ -430,35 +548,29 @@ __device__ void sweep_scale(const FusionArgs& a, const Sel& sel, const Range& rg
   v[3] = 0.0;
 }
 
+template <int U>
+__device__ void sweep_scale(const FusionArgs& a, const Sel& sel, const Range& rg,
+                            const double* ld, double ln_s, bool with_cost, double ln_s_cost,
+                            double (&v)[4], double* stage = nullptr, int stage_n = 0) {
+  sweep_scale_body<U>(rg, a.W, a.H, sel, a.dnet, a.dsemi, a.dgrad, ld, ln_s, with_cost, ln_s_cost,
+                      planes_of(a), v, stage, stage_n);
+}
+
 // scale IRLS rounds 1 and 2 from the values staged by round 0 (same
 // arithmetic, same per-thread order as sweep_scale)
 __device__ void sweep_scale_staged(const FusionArgs& a, const Range& rg, const double* stage,
                                    int stage_n, double ln_s, double (&v)[2]) {
   double num = 0.0, den = 0.0;
   for (int k = threadIdx.x; k < rg.end - rg.beg; k += FT) {
-    const double R = stage[stage_n + k];
-    if (R != -1.0) {
-      const double offset = stage[k];
-      const double wi = huber_w(offset - ln_s, a.dsemi) / R;
-      num += wi * offset;
-      den += wi;
-    }
+    const double ir = stage[stage_n + k];
+    const double offset = stage[k];
+    const double wi = huber_w(offset - ln_s, a.dsemi) * ir;
+    const bool sv = ir != -1.0;
+    num += sv ? wi * offset : 0.0;
+    den += sv ? wi : 0.0;
   }
   v[0] = num;
   v[1] = den;
-}
-
-template <class LD>
-__device__ double sweep_cost(const FusionArgs& a, const Sel& sel, const Range& rg, const LD& L,
-                             double ln_s, double* write_trial) {
-  double cost = 0.0;
-  for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) {
-    const int y = i / a.W, x = i - y * a.W;
-    const double li = L(i);
-    if (write_trial) write_trial[i] = li;
-    cost += pixel_cost(a, sel, i, x, y, L, li, ln_s);
-  }
-  return cost;
 }
 
 // assemble_normal_equations in gather form (fusion.hpp:183-219). For pixel
@@ -466,70 +578,96 @@ __device__ double sweep_cost(const FusionArgs& a, const Sel& sel, const Range& r
 // pixel: grad_y of i-W, grad_x of i-1, then net, semi, grad_x, grad_y of i.
 // Also: PCG init (r = b, z = r/diag, r.z, b.b, diag > 0 check,
 // fusion.hpp:319-332) and the depth block's c0 (fusion.hpp:429).
-__device__ void sweep_assemble(const FusionArgs& a, const Sel& sel, const Range& rg,
-                               const double* ld, double ln_s, bool store_b, double (&v)[4]) {
+template <int U>
+__device__ __forceinline__ void sweep_assemble_body(
+    const Range rg, const int W, const int H, const Sel sel, const double dnet, const double dsemi,
+    const double dgrad, const double* __restrict__ ld, const double ln_s, const SweepPlanes pl,
+    double* __restrict__ o_diag, double* __restrict__ o_right, double* __restrict__ o_down,
+    double* __restrict__ o_r, double* __restrict__ o_b, double (&v)[4]) {
   double bn = 0.0, rz = 0.0, bad = 0.0, cost = 0.0;
-  const int W = a.W, H = a.H;
-  PlainLd L{ld};
-  for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) {
-    const int y = i / W, x = i - y * W;
-    const double li = ld[i];
-    double diag = 0.0, b = 0.0, right = 0.0, down = 0.0;
-    if (sel.grad && y > 0) {
-      const int j = i - W;
-      const double r = li - ld[j] - a.pred[4][j];
-      const double wi = huber_w(r, a.dgrad) / a.pred[5][j];
-      diag += wi;
-      b -= wi * r;
+  for (int i0 = rg.beg + threadIdx.x; i0 < rg.end; i0 += U * FT) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int iu = i0 + u * FT;
+      const bool in = iu < rg.end;
+      const int i = in ? iu : rg.beg;
+      const int y = i / W, x = i - y * W;
+      const bool hasu = sel.grad && y > 0, hasl = sel.grad && x > 0;
+      const bool hasr = x + 1 < W, hasd = y + 1 < H;
+      const int ju = hasu ? i - W : i, jl = hasl ? i - 1 : i;
+      const int jr = hasr ? i + 1 : i, jd = hasd ? i + W : i;
+      const double li = ld[i], lu = ld[ju], ll = ld[jl], lr = ld[jr], ldn = ld[jd];
+      const double q0 = pl.p0[i], i0v = pl.iv0[i], q2 = pl.p2[i], i1 = pl.iv1[i];
+      const double q4 = pl.p4[i], i2 = pl.iv2[i];
+      const bool sv = pl.sval[i];
+      const double ln = pl.lns[i], ir = pl.irs[i];
+      const double q4u = pl.p4[ju], i2u = pl.iv2[ju], q2l = pl.p2[jl], i1l = pl.iv1[jl];
+      double diag = 0.0, b = 0.0, right = 0.0, down = 0.0;
+      {  // grad_y of i-W
+        const double r = li - lu - q4u;
+        const double wi = huber_w(r, dgrad) * i2u;
+        diag += hasu ? wi : 0.0;
+        b -= hasu ? wi * r : 0.0;
+      }
+      {  // grad_x of i-1
+        const double r = li - ll - q2l;
+        const double wi = huber_w(r, dgrad) * i1l;
+        diag += hasl ? wi : 0.0;
+        b -= hasl ? wi * r : 0.0;
+      }
+      if (sel.net) {
+        const double r = li - q0;
+        const double wi = huber_w(r, dnet) * i0v;
+        diag += wi;
+        b -= wi * r;
+      }
+      {  // semi
+        const double r = li - ln_s - ln;
+        const double wi = huber_w(r, dsemi) * ir;
+        diag += sv ? wi : 0.0;
+        b -= sv ? wi * r : 0.0;
+      }
+      const bool gx = sel.grad && hasr, gy = sel.grad && hasd;
+      {  // grad_x of i
+        const double r = lr - li - q2;
+        const double wi = huber_w(r, dgrad) * i1;
+        diag += gx ? wi : 0.0;
+        right -= gx ? wi : 0.0;
+        b += gx ? wi * r : 0.0;
+      }
+      {  // grad_y of i
+        const double r = ldn - li - q4;
+        const double wi = huber_w(r, dgrad) * i2;
+        diag += gy ? wi : 0.0;
+        down -= gy ? wi : 0.0;
+        b += gy ? wi * r : 0.0;
+      }
+      const double c = cost_terms(sel, hasr, hasd, li, lr, ldn, q0, i0v, sv, ln, ir, q2, i1, q4,
+                                  i2, dnet, dsemi, dgrad, ln_s);
+      if (in) {
+        o_diag[i] = diag;
+        o_right[i] = right;
+        o_down[i] = down;
+        o_r[i] = b;
+        if (o_b) o_b[i] = b;
+        bn += b * b;
+        if (!(diag > 0.0)) bad += 1.0;
+        rz += b * (b / diag);
+        cost += c;
+      }
     }
-    if (sel.grad && x > 0) {
-      const int j = i - 1;
-      const double r = li - ld[j] - a.pred[2][j];
-      const double wi = huber_w(r, a.dgrad) / a.pred[3][j];
-      diag += wi;
-      b -= wi * r;
-    }
-    if (sel.net) {
-      const double r = li - a.pred[0][i];
-      const double wi = huber_w(r, a.dnet) / a.pred[1][i];
-      diag += wi;
-      b -= wi * r;
-    }
-    if (a.svalid[i]) {
-      const double r = li - ln_s - a.lnsd[i];
-      const double R = a.semR[i];
-      const double wi = huber_w(r, a.dsemi) / R;
-      diag += wi;
-      b -= wi * r;
-    }
-    if (sel.grad && x + 1 < W) {
-      const double r = ld[i + 1] - li - a.pred[2][i];
-      const double wi = huber_w(r, a.dgrad) / a.pred[3][i];
-      diag += wi;
-      right -= wi;
-      b += wi * r;
-    }
-    if (sel.grad && y + 1 < H) {
-      const double r = ld[i + W] - li - a.pred[4][i];
-      const double wi = huber_w(r, a.dgrad) / a.pred[5][i];
-      diag += wi;
-      down -= wi;
-      b += wi * r;
-    }
-    a.diag[i] = diag;
-    a.right[i] = right;
-    a.down[i] = down;
-    a.r[i] = b;
-    if (store_b) a.b[i] = b;
-    bn += b * b;
-    if (!(diag > 0.0)) bad += 1.0;
-    rz += b * (b / diag);
-    cost += pixel_cost(a, sel, i, x, y, L, li, ln_s);
   }
   v[0] = bn;
   v[1] = rz;
   v[2] = bad;
   v[3] = cost;
+}
+
+template <int U>
+__device__ void sweep_assemble(const FusionArgs& a, const Sel& sel, const Range& rg,
+                               const double* ld, double ln_s, bool store_b, double (&v)[4]) {
+  sweep_assemble_body<U>(rg, a.W, a.H, sel, a.dnet, a.dsemi, a.dgrad, ld, ln_s, planes_of(a),
+                         a.diag, a.right, a.down, a.r, store_b ? a.b : nullptr, v);
 }
 
 // standalone PCG init from (diag, right, down, b)
@@ -681,6 +819,7 @@ __device__ __forceinline__ int pcg_solve(GridCtx& c, const FusionArgs& a, const 
 // and register allocation to the one PCG loop it runs.
 template <int PPT, int VAR>
 __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
+  constexpr int SU = PPT > 0 ? PPT : 2;  // pixels per thread per unrolled sweep group
   GridCtx c{a.slots, gridDim.x, a.base_tag, 0u, 0, 1u};
   const Range rg = my_range(a);
   const Sel sel = terms_for(a.mode);
@@ -696,21 +835,24 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
     if (threadIdx.x < 16) ctl->trace[threadIdx.x] = 0;
     __syncthreads();
   }
-  if (a.op != OP_PCG) sweep_semi_prologue(a, rg);
+  if (a.op != OP_PCG) {
+    sweep_prologue(a, rg);
+    grid_sync(c);  // fenced: sweeps read the per-call planes at i-1 and i-W
+  }
 
   if (a.op == OP_COST) {
-    double v[1] = {sweep_cost(a, sel, rg, PlainLd{a.ld[0]}, sel.scale ? log(a.scale0) : 0.0,
+    double v[1] = {sweep_cost<SU>(a, sel, rg, PlainLd{a.ld[0]}, sel.scale ? log(a.scale0) : 0.0,
                               nullptr)};
     grid_allreduce(c, v);
     if (leader) ctl->value[0] = v[0];
   } else if (a.op == OP_ASSEMBLE) {
     double v[4];
-    sweep_assemble(a, sel, rg, a.ld[0], sel.scale ? log(a.scale0) : 0.0, true, v);
+    sweep_assemble<SU>(a, sel, rg, a.ld[0], sel.scale ? log(a.scale0) : 0.0, true, v);
   } else if (a.op == OP_SCALE) {
     double ln_s = log(a.scale0);  // fusion.hpp:377
     for (int round = 0; round < 3; ++round) {
       double v[4];
-      sweep_scale(a, sel, rg, a.ld[0], ln_s, false, 0.0, v);
+      sweep_scale<SU>(a, sel, rg, a.ld[0], ln_s, false, 0.0, v);
       double w[2] = {v[0], v[1]};
       grid_allreduce(c, w);
       ln_s = w[0] / w[1];
@@ -750,17 +892,17 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
     const bool depth_solvable = !ls_mode || inliers > 0;
     int cost_evals = 0, pcg_total = 0, gn_done = 0;
     const bool otr = a.trace && leader;  // DFUSE_TRACE: ns per GN phase, CTA 0
-    __shared__ long long ot[6];          // [5] = last timestamp (thread 0 only)
+    __shared__ long long ot[8];          // [7] = last timestamp (thread 0 only)
     if (otr)
-      for (int k = 0; k < 6; ++k) ot[k] = 0;
+      for (int k = 0; k < 8; ++k) ot[k] = 0;
 #define DF_OTRACE(k)                \
   if (otr) {                        \
     const long long t_ = df_now(); \
-    ot[k] += t_ - ot[5];            \
-    ot[5] = t_;                     \
+    ot[k] += t_ - ot[7];            \
+    ot[7] = t_;                     \
   }
     for (int it = 0; it < a.gn && status == 0; ++it) {
-      if (otr) ot[5] = df_now();
+      if (otr) ot[7] = df_now();
       if (!ls_mode && a.est_scale && inliers > 0) {  // fusion.hpp:411-425
         const double ln_s0 = log(scale);
         double ln_s = ln_s0;
@@ -770,7 +912,7 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
         for (int round = 0; round < 3; ++round) {
           if (round == 0) {
             double v[4];
-            sweep_scale(a, sel, rg, a.ld[cur], ln_s, true, sel.scale ? ln_s0 : 0.0, v, stage,
+            sweep_scale<SU>(a, sel, rg, a.ld[cur], ln_s, true, sel.scale ? ln_s0 : 0.0, v, stage,
                         a.stage_n);
             double w[3] = {v[0], v[1], v[2]};
             grid_allreduce(c, w);
@@ -782,7 +924,7 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
               sweep_scale_staged(a, rg, stage, a.stage_n, ln_s, w);
             } else {
               double v[4];
-              sweep_scale(a, sel, rg, a.ld[cur], ln_s, false, 0.0, v);
+              sweep_scale<SU>(a, sel, rg, a.ld[cur], ln_s, false, 0.0, v);
               w[0] = v[0];
               w[1] = v[1];
             }
@@ -797,8 +939,9 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
         double step = 1.0, accepted = 0.0;
         for (int half = 0; half <= 5; ++half) {
           const double ts = exp(log(scale) + step * dlns);
-          double v[1] = {sweep_cost(a, sel, rg, PlainLd{a.ld[cur]}, sel.scale ? log(ts) : 0.0,
+          double v[1] = {sweep_cost<SU>(a, sel, rg, PlainLd{a.ld[cur]}, sel.scale ? log(ts) : 0.0,
                                     nullptr)};
+          DF_OTRACE(5);
           grid_allreduce(c, v);
           cost_evals += 1;
           if (v[0] <= c0) {
@@ -814,7 +957,7 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
       if (depth_solvable) {  // fusion.hpp:426-441
         const double ln_s = sel.scale ? log(scale) : 0.0;
         double v[4];
-        sweep_assemble(a, sel, rg, a.ld[cur], ln_s, false, v);
+        sweep_assemble<SU>(a, sel, rg, a.ld[cur], ln_s, false, v);
         grid_allreduce(c, v);
         const double c0 = v[3];
         cost_evals += 1;
@@ -836,9 +979,10 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
         for (int half = 0; half <= 5; ++half) {
           double w[1];
           if (xzero)
-            w[0] = sweep_cost(a, sel, rg, PlainLd{a.ld[cur]}, ln_s, a.ld[1 - cur]);
+            w[0] = sweep_cost<SU>(a, sel, rg, PlainLd{a.ld[cur]}, ln_s, a.ld[1 - cur]);
           else
-            w[0] = sweep_cost(a, sel, rg, TrialLd{a.ld[cur], a.x, step}, ln_s, a.ld[1 - cur]);
+            w[0] = sweep_cost<SU>(a, sel, rg, TrialLd{a.ld[cur], a.x, step}, ln_s, a.ld[1 - cur]);
+          DF_OTRACE(6);
           grid_allreduce(c, w);
           cost_evals += 1;
           if (w[0] <= c0) {
@@ -856,7 +1000,7 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
     }
 #undef DF_OTRACE
     if (otr)
-      for (int k = 0; k < 5; ++k) ctl->trace[8 + k] = ot[k];
+      for (int k = 0; k < 7; ++k) ctl->trace[8 + k] = ot[k];
     if (status == 0 && ls_mode) {  // fusion.hpp:445-452
       double v[1] = {0.0};
       const double* ld = a.ld[cur];
@@ -900,7 +1044,6 @@ __global__ void __launch_bounds__(FT, 1) k_gradient(FusionArgs a, double* g) {
   const int W = a.W, H = a.H;
   const double* ld = a.ld[0];
   PlainLd L{ld};
-  sweep_semi_prologue(a, rg);
   double cost = 0.0, gs = 0.0;
   for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) {
     const int y = i / W, x = i - y * W;
@@ -921,8 +1064,8 @@ __global__ void __launch_bounds__(FT, 1) k_gradient(FusionArgs a, double* g) {
       gi += 2.0 * huber_w(r, a.dnet) * r / a.pred[1][i];
     }
     if (a.svalid[i]) {
-      const double R = a.semR[i];
-      const double r = li - ln_s - a.lnsd[i];
+      const double R = semi_logvar(a.sv[i], a.sd[i]);  // fusion.hpp:95-100
+      const double r = li - ln_s - log(a.sd[i]);
       const double d = 2.0 * huber_w(r, a.dsemi) * r / R;
       gi += d;
       if (sel.scale) gs -= d;
@@ -936,7 +1079,7 @@ __global__ void __launch_bounds__(FT, 1) k_gradient(FusionArgs a, double* g) {
       gi -= 2.0 * huber_w(r, a.dgrad) * r / a.pred[5][i];
     }
     g[i] = gi;
-    cost += pixel_cost(a, sel, i, x, y, L, li, ln_s);
+    cost += pixel_cost_exact(a, sel, i, x, y, L, li, ln_s);
   }
   double v[2] = {cost, gs};
   grid_allreduce(c, v);
@@ -1118,9 +1261,9 @@ void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
     fprintf(stderr,
             "dfuse trace (ppt %d, ns, CTA 0): ring %.0f spmv %.0f ar/wait_rz %.0f pq_upd %.0f "
             "ar_pq %.0f sweep %.0f | scale %lld strial %lld assemble %lld pcg %lld dtrial %lld "
-            "(pcg its %d) sm_clock %.0f MHz\n",
+            "(pcg its %d) sm_clock %.0f MHz | trial sweeps only: scale %lld depth %lld\n",
             a.ppt, ns[0], ns[1], ns[2], ns[3], ns[4], ns[5], tr[8], tr[9], tr[10], tr[11], tr[12],
-            its, 1e3 * ghz);
+            its, 1e3 * ghz, tr[13], tr[14]);
     if (a.dbg && ctx->trace >= 3) {  // each CTA's view of its all-reduces (SM cycles)
       std::vector<long long> h(dbg_n);
       DF_CUDA(cudaMemcpy(h.data(), a.dbg, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost));

@@ -39,8 +39,10 @@ struct FusionArgs {
   const double* sd;
   const double* sv;
   const uint8_t* svalid;
-  double* lnsd;  // log(semi depth), filled by the kernel prologue (valid pixels)
-  double* semR;  // semi_log_variance(variance, depth), same
+  // per-call planes, filled by the kernel prologue (sweep_prologue)
+  double* lnsd;     // log(semi depth), 0 where the semi map has no value
+  double* irs;      // 1 / semi_log_variance(variance, depth), 0 likewise
+  double* ivar[3];  // 1 / log_depth_var, 1 / grad_x_var, 1 / grad_y_var
   int inlier_count;
   const int* inlier_dev;  // if set, overrides inlier_count (device-resident session)
   double dsemi, dnet, dgrad, cg_tol;

@@ -171,7 +171,7 @@ int dfuse_kf_create(dfuse_ctx* ctx, const dfuse_intrinsics* K, const float* I0,
     const size_t dP = al(sizeof(double) * P);
     const bool resident = fusion_resident_possible(P, kf->grid);
     const size_t total = 2 * al(sizeof(float) * P) + al(P) + al(sizeof(int) * P) + 2 * dP +
-                         al(P) + 256 + 8 * dP + 11 * dP + al(fusion_slots_bytes(kf->grid)) +
+                         al(P) + 256 + 11 * dP + 11 * dP + al(fusion_slots_bytes(kf->grid)) +
                          al(sizeof(FusionControl)) + al(2 * sizeof(FusionStateDev)) +
                          (resident ? al(fusion_halo_bytes(P)) : 0);
     DF_CUDA(cudaMalloc(&kf->block, total));
@@ -198,7 +198,8 @@ int dfuse_kf_create(dfuse_ctx* ctx, const dfuse_intrinsics* K, const float* I0,
     f.sv = kf->semi_v;
     f.svalid = kf->semi_valid;
     f.lnsd = (double*)take(dP);
-    f.semR = (double*)take(dP);
+    f.irs = (double*)take(dP);
+    for (int k = 0; k < 3; ++k) f.ivar[k] = (double*)take(dP);
     f.inlier_dev = kf->counters + 4;
     f.ld[0] = (double*)take(dP);
     f.ld[1] = (double*)take(dP);
