@@ -903,19 +903,23 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
   }
     for (int it = 0; it < a.gn && status == 0; ++it) {
       if (otr) ot[7] = df_now();
+      bool have_eq = false;  // the scale block left an assembly valid for the depth block
+      double veq[4] = {0.0, 0.0, 0.0, 0.0};
       if (!ls_mode && a.est_scale && inliers > 0) {  // fusion.hpp:411-425
         const double ln_s0 = log(scale);
         double ln_s = ln_s0;
         double c0 = 0.0;
         extern __shared__ double dsm_stage[];
         double* stage = a.stage_n > 0 ? dsm_stage : nullptr;
+        // the scale sweeps write no global memory, so their all-reduces need
+        // no fence
         for (int round = 0; round < 3; ++round) {
           if (round == 0) {
             double v[4];
             sweep_scale<SU>(a, sel, rg, a.ld[cur], ln_s, true, sel.scale ? ln_s0 : 0.0, v, stage,
-                        a.stage_n);
+                            a.stage_n);
             double w[3] = {v[0], v[1], v[2]};
-            grid_allreduce(c, w);
+            grid_allreduce<3, false>(c, w);
             c0 = w[2];
             ln_s = w[0] / w[1];
           } else {
@@ -928,7 +932,7 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
               w[0] = v[0];
               w[1] = v[1];
             }
-            grid_allreduce(c, w);
+            grid_allreduce<2, false>(c, w);
             ln_s = w[0] / w[1];
           }
         }
@@ -939,12 +943,30 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
         double step = 1.0, accepted = 0.0;
         for (int half = 0; half <= 5; ++half) {
           const double ts = exp(log(scale) + step * dlns);
-          double v[1] = {sweep_cost<SU>(a, sel, rg, PlainLd{a.ld[cur]}, sel.scale ? log(ts) : 0.0,
-                                    nullptr)};
-          DF_OTRACE(5);
-          grid_allreduce(c, v);
+          double tc;
+          if (half == 0 && depth_solvable) {
+            // The full step is accepted almost always, and the depth block
+            // then assembles at exactly this (state, scale) and starts from
+            // exactly this cost (fusion.hpp:426-429). So the first trial's
+            // sweep assembles the normal equations speculatively; its cost
+            // is the trial cost, and on acceptance the assembly stands.
+            double v[4];
+            sweep_assemble<SU>(a, sel, rg, a.ld[cur], sel.scale ? log(ts) : 0.0, false, v);
+            grid_allreduce(c, v);  // fenced: the PCG reads the assembled rasters
+            tc = v[3];
+            if (tc <= c0) {
+              have_eq = true;
+              for (int k = 0; k < 4; ++k) veq[k] = v[k];
+            }
+          } else {
+            double v[1] = {sweep_cost<SU>(a, sel, rg, PlainLd{a.ld[cur]},
+                                          sel.scale ? log(ts) : 0.0, nullptr)};
+            DF_OTRACE(5);
+            grid_allreduce<1, false>(c, v);
+            tc = v[0];
+          }
           cost_evals += 1;
-          if (v[0] <= c0) {
+          if (tc <= c0) {
             scale = ts;
             accepted = step;
             break;
@@ -957,8 +979,12 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
       if (depth_solvable) {  // fusion.hpp:426-441
         const double ln_s = sel.scale ? log(scale) : 0.0;
         double v[4];
-        sweep_assemble<SU>(a, sel, rg, a.ld[cur], ln_s, false, v);
-        grid_allreduce(c, v);
+        if (have_eq) {  // assembled by the accepted scale trial
+          for (int k = 0; k < 4; ++k) v[k] = veq[k];
+        } else {
+          sweep_assemble<SU>(a, sel, rg, a.ld[cur], ln_s, false, v);
+          grid_allreduce(c, v);
+        }
         const double c0 = v[3];
         cost_evals += 1;
         DF_OTRACE(2);
