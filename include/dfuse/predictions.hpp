@@ -1,8 +1,9 @@
 // dfuse/predictions.hpp -- drop-in for the solver input of
 // proj/include/dfuse/predictions.hpp:18-29 (PredictionSet: six rasters of
-// float32-exact doubles) and focal_adjust (148-157). DFPRED file I/O and the
-// synthetic oracle are per-keyframe tooling outside the per-frame hot path
-// and are not part of this drop-in yet.
+// float32-exact doubles) and focal_adjust (148-157). A DFPRED file goes
+// straight to the device: DeviceKeyframe(K, I0, path, threshold) in
+// dfuse/session.hpp runs load_predictions' checks and focal_adjust there
+// (SURVEY.md 8(f) f2). The synthetic oracle is test tooling, not drop-in.
 #pragma once
 
 #include <cmath>

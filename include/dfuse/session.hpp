@@ -1,7 +1,9 @@
 // dfuse/session.hpp -- the device-resident keyframe (replaces the hot part of
-// proj/include/dfuse/pipeline.hpp: make_keyframe 125-153 minus prediction
-// I/O, and process_frame 194-228 for tracked frames with retirement decided
-// by the caller).
+// proj/include/dfuse/pipeline.hpp: make_keyframe 125-153, from prediction
+// planes or from a DFPRED file (load_predictions + focal_adjust on the
+// device), and process_frame 194-228 for tracked frames; the retirement test
+// should_create_keyframe (215-218) with the median predicted depth cached on
+// the device).
 //
 //   dfuse::DeviceKeyframe kf(K, I0, predictions, cfg.texture_threshold);
 //   auto r = kf.process_frame(kf_pose, frame_pose, frame.intensity,
@@ -11,7 +13,13 @@
 //   FusionState st = kf.fusion();  SemiDenseMap m = kf.semidense();
 #pragma once
 
+#include <fstream>
+#include <iterator>
+#include <string>
+#include <vector>
+
 #include "dfuse/fusion.hpp"
+#include "dfuse/semidense.hpp"
 
 namespace dfuse {
 
@@ -38,7 +46,42 @@ class DeviceKeyframe {
                                   texture_threshold, &kf_),
                   "make_keyframe");
   }
+  // make_keyframe with cfg.predictions_dir set (pipeline.hpp:133-147): the
+  // DFPRED file at `dfpred_path` is read here and validated, widened and
+  // focal-adjusted to K.fx on the device
+  DeviceKeyframe(const CameraIntrinsics& K, const IntensityImage& I0,
+                 const std::string& dfpred_path, double texture_threshold)
+      : K_(K) {
+    std::ifstream in(dfpred_path, std::ios::binary);
+    if (!in) throw Error(Err::MissingFile, dfpred_path);  // predictions.hpp:70-71
+    const std::vector<char> bytes((std::istreambuf_iterator<char>(in)),
+                                  std::istreambuf_iterator<char>());
+    const dfuse_intrinsics k = K.c_abi();
+    device::check(dfuse_kf_create_dfpred(device::ctx(), &k, I0.raster().data(), bytes.data(),
+                                         bytes.size(), texture_threshold, &kf_),
+                  dfpred_path.c_str());
+  }
   ~DeviceKeyframe() { dfuse_kf_destroy(kf_); }
+
+  // detail::median_predicted_depth (pipeline.hpp:94-99), once per keyframe
+  double median_depth() const {
+    double m = 0.0;
+    device::check(dfuse_kf_median_depth(kf_, &m), "median_predicted_depth");
+    return m;
+  }
+
+  // process_frame's retirement test (pipeline.hpp:215-218) for the frame at
+  // `frame_pose`, after its process_frame call
+  bool should_create_keyframe(const Pose& keyframe_pose, const Pose& frame_pose,
+                              const KeyframePolicy& policy = {}) const {
+    SemiDenseMap m;
+    int32_t count = 0;
+    device::check(dfuse_kf_download(kf_, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                    &count, nullptr),
+                  "download");
+    m.inlier_count = count;
+    return dfuse::should_create_keyframe(keyframe_pose, frame_pose, median_depth(), m, policy);
+  }
   DeviceKeyframe(const DeviceKeyframe&) = delete;
   DeviceKeyframe& operator=(const DeviceKeyframe&) = delete;
 

@@ -19,6 +19,7 @@
 #ifndef DFUSE_CUDA_H
 #define DFUSE_CUDA_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -258,7 +259,47 @@ typedef struct {
  * semi-dense map and sets the fusion state to init_state(pred). */
 int dfuse_kf_create(dfuse_ctx* ctx, const dfuse_intrinsics* K, const float* I0,
                     const double* const pred[6], double texture_threshold, dfuse_keyframe** out);
+/* make_keyframe with a DFPRED prediction file already in host memory
+ * (pipeline.hpp:133-147): load_predictions' checks (predictions.hpp:69-123;
+ * header on the host, same codes and byte offsets in the messages; the
+ * variance check on the device, first failure in file order), the size check
+ * against K (DimensionMismatch), focal_adjust to K->fx (predictions.hpp:148-157)
+ * on the device, then as dfuse_kf_create. The six fp32 planes are copied to
+ * HBM as they are (24 B/px) and widened there. */
+int dfuse_kf_create_dfpred(dfuse_ctx* ctx, const dfuse_intrinsics* K, const float* I0,
+                           const void* dfpred, size_t nbytes, double texture_threshold,
+                           dfuse_keyframe** out);
+/* DFPRED header checks alone (predictions.hpp:72-95); host code, ctx may be
+ * NULL (then no message) */
+int dfuse_dfpred_header(dfuse_ctx* ctx, const void* bytes, size_t nbytes, int32_t* width,
+                        int32_t* height, double* source_focal);
+/* median_predicted_depth (pipeline.hpp:94-99) of the keyframe's predictions,
+ * computed once on the device (exact selection) and cached: the per-frame
+ * should_create_keyframe test (semidense.hpp:419-424) needs only this and
+ * the inlier count */
+int dfuse_kf_median_depth(dfuse_keyframe* kf, double* median_depth);
 int dfuse_kf_destroy(dfuse_keyframe* kf);
+
+/* ---- scoring (eval.hpp:34-68, 221-226; pipeline.hpp:232-247) --------- */
+typedef struct {
+  double pct_within_10;   /* KeyframeScore::pct_correct */
+  int32_t n_evaluated;    /* valid ground-truth pixels (finalize_keyframe's n_gt) */
+  double median_abs_rel;  /* KeyframeScore::median_abs_rel */
+} dfuse_keyframe_score;
+/* pct_within_10 + median_abs_rel of an estimate in metres against ground
+ * truth (host buffers; est_valid may be NULL = every estimate defined).
+ * NoValidGroundTruth on an empty ground-truth mask (eval.hpp:45). */
+int dfuse_score_depth(dfuse_ctx* ctx, int width, int height, const double* est,
+                      const uint8_t* est_valid, const double* gt_metres, const uint8_t* gt_valid,
+                      dfuse_keyframe_score* out);
+/* finalize_keyframe's score of the session's fused state, est = exp(log_depth)
+ * computed on the device (pipeline.hpp:234-247); gt on the host */
+int dfuse_kf_score(dfuse_keyframe* kf, const double* gt_metres, const uint8_t* gt_valid,
+                   dfuse_keyframe_score* out);
+/* export_depth_image's 16-bit raster of the session's fused state:
+ * round(exp(log_depth) * depth_scale) clamped to [0, 65535]
+ * (eval.hpp:221-226, depth_io.hpp:51-63); PNG encoding is the caller's */
+int dfuse_kf_export_depth_u16(dfuse_keyframe* kf, double depth_scale, uint16_t* out);
 /* restore the just-created state (device-to-device copies) */
 int dfuse_kf_reset(dfuse_keyframe* kf);
 /* process_frame for a tracked frame: stereo scan + update + optimize.

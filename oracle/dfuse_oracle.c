@@ -986,3 +986,77 @@ int orc_should_create_keyframe(const double q_kf[4], const double t_kf[3], const
   *out = trans / median > lambda_trans || inlier_count < lambda_inliers;
   return DFUSE_OK;
 }
+
+/* focal_adjust, predictions.hpp:148-157: log_depth += log(test/source)
+ * unless the focal lengths are equal */
+int orc_focal_adjust(int w, int h, double* log_depth, double source_focal, double test_focal) {
+  if (test_focal <= 0.0 || source_focal <= 0.0) return DFUSE_E_NON_POSITIVE_FOCAL;
+  if (test_focal == source_focal) return DFUSE_OK;
+  const double shift = log(test_focal / source_focal);
+  for (long i = 0; i < (long)w * h; ++i) log_depth[i] += shift;
+  return DFUSE_OK;
+}
+
+static int cmp_double(const void* a, const void* b) {
+  const double x = *(const double*)a, y = *(const double*)b;
+  return (x > y) - (x < y);
+}
+
+/* detail::median_predicted_depth, pipeline.hpp:94-99: exp of the element
+ * std::nth_element places at n/2 (= the (n/2)-th smallest) */
+double orc_median_predicted_depth(const double* log_depth, long n) {
+  double* v = (double*)malloc(sizeof(double) * (size_t)n);
+  memcpy(v, log_depth, sizeof(double) * (size_t)n);
+  qsort(v, (size_t)n, sizeof(double), cmp_double);
+  const double m = v[n / 2];
+  free(v);
+  return exp(m);
+}
+
+/* pct_within_10 (eval.hpp:34-46): 100 * correct / valid-gt, with the
+ * boundary-inclusive 0.10 + 1e-12 threshold (eval.hpp:29); NULL est_valid =
+ * every estimate defined. Returns NoValidGroundTruth on an empty gt mask. */
+int orc_pct_within_10(long n, const double* est, const uint8_t* est_valid, const double* gt,
+                      const uint8_t* gt_valid, double* out) {
+  long n_gt = 0, n_ok = 0;
+  for (long i = 0; i < n; ++i) {
+    if (!gt_valid[i]) continue;
+    ++n_gt;
+    if (est_valid && !est_valid[i]) continue;
+    if (fabs(est[i] - gt[i]) / gt[i] <= 0.10 + 1e-12) ++n_ok;
+  }
+  if (n_gt == 0) return DFUSE_E_NO_VALID_GROUND_TRUTH;
+  *out = 100.0 * (double)n_ok / (double)n_gt;
+  return DFUSE_OK;
+}
+
+/* median_abs_rel (eval.hpp:52-68): the element nth_element puts at n/2 of
+ * |est - gt| / gt over pixels where both are defined; 0 when there are none */
+double orc_median_abs_rel(long n, const double* est, const uint8_t* est_valid, const double* gt,
+                          const uint8_t* gt_valid) {
+  double* r = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  long m = 0;
+  for (long i = 0; i < n; ++i) {
+    if (!gt_valid[i]) continue;
+    if (est_valid && !est_valid[i]) continue;
+    r[m++] = fabs(est[i] - gt[i]) / gt[i];
+  }
+  double out = 0.0;
+  if (m > 0) {
+    qsort(r, (size_t)m, sizeof(double), cmp_double);
+    out = r[m / 2];
+  }
+  free(r);
+  return out;
+}
+
+/* export_depth_image (eval.hpp:221-226) through save_depth_png's
+ * quantisation (depth_io.hpp:61-62): round(exp(ld) * scale) clamped to
+ * [0, 65535] */
+void orc_export_depth_u16(long n, const double* log_depth, double depth_scale, uint16_t* out) {
+  for (long i = 0; i < n; ++i) {
+    double s = round(exp(log_depth[i]) * depth_scale);
+    s = s < 0.0 ? 0.0 : (s > 65535.0 ? 65535.0 : s);
+    out[i] = (uint16_t)s;
+  }
+}

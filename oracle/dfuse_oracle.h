@@ -95,6 +95,19 @@ int ref_process_frame(const dfuse_epigeom* g, const float* I0, const float* I1,
                       double* stereo_ms, double* optimise_ms);
 int ref_omp_max_threads(void);
 
+/* focal_adjust (predictions.hpp:148-157), median_predicted_depth
+ * (pipeline.hpp:94-99) */
+int orc_focal_adjust(int w, int h, double* log_depth, double source_focal, double test_focal);
+double orc_median_predicted_depth(const double* log_depth, long n);
+
+/* scoring: pct_within_10, median_abs_rel (eval.hpp:34-68), export_depth_image
+ * quantisation (eval.hpp:221-226, depth_io.hpp:51-63) */
+int orc_pct_within_10(long n, const double* est, const uint8_t* est_valid, const double* gt,
+                      const uint8_t* gt_valid, double* out);
+double orc_median_abs_rel(long n, const double* est, const uint8_t* est_valid, const double* gt,
+                          const uint8_t* gt_valid);
+void orc_export_depth_u16(long n, const double* log_depth, double depth_scale, uint16_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,6 +15,7 @@
 #include <optional>
 #include <vector>
 
+#include "dfuse/eval.hpp"
 #include "dfuse/fusion.hpp"
 #include "dfuse/predictions.hpp"
 #include "dfuse/semidense.hpp"
@@ -507,6 +508,120 @@ int ref_should_create_keyframe(const double q_kf[4], const double t_kf[3], const
     m.inlier_count = inlier_count;
     *out = should_create_keyframe(make_pose(q_kf, t_kf), make_pose(q_cur, t_cur), median, m,
                                   KeyframePolicy{lambda_trans, lambda_inliers});
+    return DFUSE_OK;
+  } catch (const Error& e) {
+    return code_of(e);
+  }
+}
+
+// ---- prediction files (predictions.hpp:69-157), for the DFPRED ingest pin
+namespace {
+void copy_msg(const Error& e, char* msg, int msglen) {
+  if (msg && msglen > 0) {
+    std::strncpy(msg, e.what(), (size_t)msglen - 1);
+    msg[msglen - 1] = 0;
+  }
+}
+}  // namespace
+
+int ref_load_predictions(const char* path, int w, int h, double* planes, double* source_focal,
+                         char* msg, int msglen) {
+  try {
+    const PredictionSet p = load_predictions(path);
+    if (p.width() != w || p.height() != h) return DFUSE_E_DIMENSION_MISMATCH;
+    const Raster<double>* ch[6] = {&p.log_depth, &p.log_depth_var, &p.grad_x,
+                                   &p.grad_x_var, &p.grad_y,       &p.grad_y_var};
+    const std::size_t n = (std::size_t)w * h;
+    for (int c = 0; c < 6; ++c) std::memcpy(planes + c * n, ch[c]->data(), n * sizeof(double));
+    *source_focal = p.source_focal;
+    return DFUSE_OK;
+  } catch (const Error& e) {
+    copy_msg(e, msg, msglen);
+    return code_of(e);
+  }
+}
+
+int ref_save_predictions(const char* path, int w, int h, const double* planes,
+                         double source_focal) {
+  try {
+    PredictionSet p;
+    Raster<double>* ch[6] = {&p.log_depth, &p.log_depth_var, &p.grad_x,
+                             &p.grad_x_var, &p.grad_y,       &p.grad_y_var};
+    const std::size_t n = (std::size_t)w * h;
+    for (int c = 0; c < 6; ++c) {
+      *ch[c] = Raster<double>(w, h, 0.0);
+      std::memcpy(ch[c]->data(), planes + c * n, n * sizeof(double));
+    }
+    p.source_focal = source_focal;
+    save_predictions(p, path);
+    return DFUSE_OK;
+  } catch (const Error& e) {
+    return code_of(e);
+  }
+}
+
+int ref_focal_adjust(int w, int h, double* log_depth, double source_focal, double test_focal) {
+  try {
+    PredictionSet p;
+    p.log_depth = Raster<double>(w, h, 0.0);
+    std::memcpy(p.log_depth.data(), log_depth, sizeof(double) * (std::size_t)w * h);
+    p.source_focal = source_focal;
+    const PredictionSet q = focal_adjust(p, test_focal);
+    std::memcpy(log_depth, q.log_depth.data(), sizeof(double) * (std::size_t)w * h);
+    return DFUSE_OK;
+  } catch (const Error& e) {
+    return code_of(e);
+  }
+}
+
+// ---- scoring (eval.hpp:34-68, 221-226; pipeline.hpp:232-247) ------------
+namespace {
+DepthImage depth_image(int w, int h, const double* gt, const uint8_t* gt_valid) {
+  DepthImage d{Raster<double>(w, h, 0.0), Mask(w, h, 0)};
+  std::memcpy(d.metres.data(), gt, sizeof(double) * (std::size_t)w * h);
+  std::memcpy(d.valid.data(), gt_valid, (std::size_t)w * h);
+  return d;
+}
+}  // namespace
+
+int ref_pct_within_10(int w, int h, const double* est, const uint8_t* est_valid,
+                      const double* gt, const uint8_t* gt_valid, double* out) {
+  try {
+    Raster<double> e(w, h, 0.0);
+    std::memcpy(e.data(), est, sizeof(double) * (std::size_t)w * h);
+    Mask m(w, h, 0);
+    if (est_valid) std::memcpy(m.data(), est_valid, (std::size_t)w * h);
+    *out = pct_within_10(e, est_valid ? &m : nullptr, depth_image(w, h, gt, gt_valid));
+    return DFUSE_OK;
+  } catch (const Error& e) {
+    return code_of(e);
+  }
+}
+
+int ref_median_abs_rel(int w, int h, const double* est, const uint8_t* est_valid,
+                       const double* gt, const uint8_t* gt_valid, double* out) {
+  try {
+    Raster<double> e(w, h, 0.0);
+    std::memcpy(e.data(), est, sizeof(double) * (std::size_t)w * h);
+    Mask m(w, h, 0);
+    if (est_valid) std::memcpy(m.data(), est_valid, (std::size_t)w * h);
+    *out = median_abs_rel(e, est_valid ? &m : nullptr, depth_image(w, h, gt, gt_valid));
+    return DFUSE_OK;
+  } catch (const Error& e) {
+    return code_of(e);
+  }
+}
+
+// export_depth_image (eval.hpp:221-226) -> save_depth_png's 16-bit raster,
+// captured by the in-memory imwrite of oracle/compat_cv
+int ref_export_depth_u16(int w, int h, const double* log_depth, double depth_scale,
+                         uint16_t* out) {
+  try {
+    FusionState st{Raster<double>(w, h, 0.0), 1.0, 0};
+    std::memcpy(st.log_depth.data(), log_depth, sizeof(double) * (std::size_t)w * h);
+    export_depth_image(st, "ref_export.png", depth_scale);
+    const cv::Mat& m = cv::image_store().at("ref_export.png");
+    for (int y = 0; y < h; ++y) std::memcpy(out + (std::size_t)y * w, m.ptr<uint16_t>(y), 2 * w);
     return DFUSE_OK;
   } catch (const Error& e) {
     return code_of(e);

@@ -56,6 +56,16 @@ def lib() -> C.CDLL:
             f.argtypes = [C.c_void_p, C.POINTER(EpiGeom), C.c_void_p, C.c_void_p, C.c_void_p,
                           C.c_int, C.POINTER(FrameResultC)]
         L.dfuse_kf_download.argtypes = [C.c_void_p] + [C.c_void_p] * 8
+        L.dfuse_kf_create_dfpred.argtypes = [C.c_void_p, C.POINTER(Intrinsics), C.c_void_p,
+                                             C.c_char_p, C.c_size_t, C.c_double,
+                                             C.POINTER(C.c_void_p)]
+        L.dfuse_dfpred_header.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t,
+                                          C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                          C.POINTER(C.c_double)]
+        L.dfuse_kf_median_depth.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+        L.dfuse_score_depth.argtypes = [C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 5
+        L.dfuse_kf_score.argtypes = [C.c_void_p] + [C.c_void_p] * 3
+        L.dfuse_kf_export_depth_u16.argtypes = [C.c_void_p, C.c_double, C.c_void_p]
         _lib = L
     return _lib
 
@@ -123,25 +133,88 @@ def cuda(device: int = 0) -> Bindings:
     return context(device).api
 
 
+class KeyframeScoreC(C.Structure):  # dfuse_keyframe_score
+    _fields_ = [("pct_within_10", C.c_double), ("n_evaluated", C.c_int32),
+                ("median_abs_rel", C.c_double)]
+
+
+def score_depth(ctx: "Context", est, gt_metres, gt_valid, est_valid=None) -> KeyframeScoreC:
+    """pct_within_10 + median_abs_rel (eval.hpp:34-68) on the device."""
+    est = _f64(est)
+    gt = _f64(gt_metres)
+    gv = np.ascontiguousarray(gt_valid, np.uint8)
+    ev = None if est_valid is None else np.ascontiguousarray(est_valid, np.uint8)
+    h, w = est.shape
+    out = KeyframeScoreC()
+    L = lib()
+    rc = L.dfuse_score_depth(ctx.handle, w, h, est.ctypes.data,
+                             None if ev is None else ev.ctypes.data, gt.ctypes.data,
+                             gv.ctypes.data, C.byref(out))
+    if rc != 0:
+        raise DfuseError(rc, L.dfuse_last_error(ctx.handle).decode())
+    return out
+
+
+def dfpred_header(data: bytes):
+    """load_predictions' header checks (predictions.hpp:72-95), host code in
+    the library (no device needed) -> (width, height, source_focal)."""
+    L = lib()
+    w, h, f = C.c_int32(0), C.c_int32(0), C.c_double(0.0)
+    rc = L.dfuse_dfpred_header(None, data, len(data), C.byref(w), C.byref(h), C.byref(f))
+    if rc != 0:
+        raise DfuseError(rc, "dfuse_dfpred_header")
+    return w.value, h.value, f.value
+
+
 class Keyframe:
     """Device-resident keyframe (dfuse_keyframe): make_keyframe on creation,
     process_frame per tracked frame, download() for the state."""
 
-    def __init__(self, ctx: Context, camera, I0, pred: PredictionSet,
-                 texture_threshold: float = 0.02):
+    def __init__(self, ctx: Context, camera, I0, pred: PredictionSet | None,
+                 texture_threshold: float = 0.02, dfpred: bytes | None = None):
+        """`pred`: the prediction planes (already focal-adjusted), or
+        `dfpred`: the bytes of a DFPRED file (make_keyframe's
+        load_predictions + focal_adjust to camera.fx, on the device)."""
         L = lib()
         self.ctx = ctx
         self.W, self.H = camera.width, camera.height
         self._I0 = _f32(I0)
-        self._planes = pred.planes()
-        arr = (C.c_void_p * 6)(*[p.ctypes.data for p in self._planes])
         kc = camera.c()
         h = C.c_void_p()
-        rc = L.dfuse_kf_create(ctx.handle, C.byref(kc), self._I0.ctypes.data, arr,
-                               float(texture_threshold), C.byref(h))
+        if dfpred is not None:
+            rc = L.dfuse_kf_create_dfpred(ctx.handle, C.byref(kc), self._I0.ctypes.data,
+                                          bytes(dfpred), len(dfpred), float(texture_threshold),
+                                          C.byref(h))
+        else:
+            self._planes = pred.planes()
+            arr = (C.c_void_p * 6)(*[p.ctypes.data for p in self._planes])
+            rc = L.dfuse_kf_create(ctx.handle, C.byref(kc), self._I0.ctypes.data, arr,
+                                   float(texture_threshold), C.byref(h))
         if rc != 0:
             raise DfuseError(rc, L.dfuse_last_error(ctx.handle).decode())
         self.handle = h
+
+    def score(self, gt_metres, gt_valid) -> KeyframeScoreC:
+        """finalize_keyframe's score of the fused state (pipeline.hpp:232-247)"""
+        gt = _f64(gt_metres)
+        gv = np.ascontiguousarray(gt_valid, np.uint8)
+        out = KeyframeScoreC()
+        self._check(lib().dfuse_kf_score(self.handle, gt.ctypes.data, gv.ctypes.data,
+                                         C.byref(out)), "dfuse_kf_score")
+        return out
+
+    def export_depth_u16(self, depth_scale: float = 5000.0) -> np.ndarray:
+        """export_depth_image's 16-bit raster (eval.hpp:221-226)"""
+        out = np.zeros((self.H, self.W), np.uint16)
+        self._check(lib().dfuse_kf_export_depth_u16(self.handle, float(depth_scale),
+                                                    out.ctypes.data), "dfuse_kf_export_depth_u16")
+        return out
+
+    def median_depth(self) -> float:
+        """median_predicted_depth (pipeline.hpp:94-99), cached on the device"""
+        v = C.c_double(0.0)
+        self._check(lib().dfuse_kf_median_depth(self.handle, C.byref(v)), "dfuse_kf_median_depth")
+        return v.value
 
     def _check(self, rc, what):
         if rc != 0:

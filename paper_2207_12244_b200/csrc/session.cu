@@ -7,11 +7,15 @@
 // between them: the inlier count and the fusion state scalars (scale,
 // iteration, live log-depth buffer) stay on the device. One small
 // device->host copy per frame returns the ProcessOutcome-like result.
+#include <math.h>
 #include <string.h>
 
+#include <cub/device/device_radix_sort.cuh>
 #include <new>
+#include <string>
 
 #include "common.cuh"
+#include "eval.cuh"
 #include "fusion.cuh"
 #include "stereo.cuh"
 
@@ -38,6 +42,7 @@ struct dfuse_keyframe {
   FusionStateDev* st = nullptr;  // [2] ping-pong
   FusionControl* h_ctl = nullptr;  // pinned
   int* h_counters = nullptr;       // pinned
+  double median_depth = -1.0;      // cached median_predicted_depth (< 0: not computed)
 };
 
 namespace {
@@ -145,6 +150,150 @@ void process(dfuse_keyframe* kf, const dfuse_epigeom* g, const float* I1_dev,
   res->stats = kf->h_ctl->stats;
 }
 
+// the session's one device allocation (make_keyframe's Keyframe, the
+// fusion workspace and its control blocks)
+void kf_alloc(dfuse_keyframe* kf, const dfuse_intrinsics* K) {
+  dfuse_ctx* ctx = kf->ctx;
+  kf->W = K->width;
+  kf->H = K->height;
+  const long P = kf->P = (long)kf->W * kf->H;
+  kf->grid = fusion_grid(ctx);
+  const size_t dP = al(sizeof(double) * P);
+  const bool resident = fusion_resident_possible(P, kf->grid);
+  const size_t total = 2 * al(sizeof(float) * P) + al(P) + al(sizeof(int) * P) + 2 * dP +
+                       al(P) + 256 + 11 * dP + 11 * dP + al(fusion_slots_bytes(kf->grid)) +
+                       al(sizeof(FusionControl)) + al(2 * sizeof(FusionStateDev)) +
+                       (resident ? al(fusion_halo_bytes(P)) : 0);
+  DF_CUDA(cudaMalloc(&kf->block, total));
+  char* p = (char*)kf->block;
+  auto take = [&](size_t bytes) {
+    char* r = p;
+    p += al(bytes);
+    return (void*)r;
+  };
+  kf->I0 = (float*)take(sizeof(float) * P);
+  kf->I1 = (float*)take(sizeof(float) * P);
+  kf->mask = (uint8_t*)take(P);
+  kf->list = (int*)take(sizeof(int) * P);
+  kf->semi_d = (double*)take(dP);
+  kf->semi_v = (double*)take(dP);
+  kf->semi_valid = (uint8_t*)take(P);
+  kf->counters = (int*)take(256);
+  FusionArgs& f = kf->fa;
+  memset(&f, 0, sizeof f);
+  f.W = kf->W;
+  f.H = kf->H;
+  for (int c = 0; c < 6; ++c) f.pred[c] = (double*)take(dP);
+  f.sd = kf->semi_d;
+  f.sv = kf->semi_v;
+  f.svalid = kf->semi_valid;
+  f.lnsd = (double*)take(dP);
+  f.irs = (double*)take(dP);
+  for (int k = 0; k < 3; ++k) f.ivar[k] = (double*)take(dP);
+  f.inlier_dev = kf->counters + 4;
+  f.ld[0] = (double*)take(dP);
+  f.ld[1] = (double*)take(dP);
+  f.diag = (double*)take(dP);
+  f.right = (double*)take(dP);
+  f.down = (double*)take(dP);
+  f.b = (double*)take(dP);
+  f.x = (double*)take(dP);
+  f.r = (double*)take(dP);
+  f.p[0] = (double*)take(dP);
+  f.p[1] = (double*)take(dP);
+  f.q = (double*)take(dP);
+  f.slots = (ReduceSlot*)take(fusion_slots_bytes(kf->grid));
+  f.halo = resident ? (unsigned long long*)take(fusion_halo_bytes(P)) : nullptr;
+  f.ctl = (FusionControl*)take(sizeof(FusionControl));
+  kf->st = (FusionStateDev*)take(2 * sizeof(FusionStateDev));
+  DF_CUDA(cudaMallocHost(&kf->h_ctl, sizeof(FusionControl)));
+  DF_CUDA(cudaMallocHost(&kf->h_counters, 8 * sizeof(int)));
+  DF_CUDA(cudaMemsetAsync(kf->counters, 0, 256, ctx->stream));
+}
+
+// upload I0, texture mask (pipeline.hpp:148) + the masked-pixel list, empty
+// semi-dense map and init_state (pipeline.hpp:149-150)
+void kf_finish(dfuse_keyframe* kf, const float* I0, double texture_threshold) {
+  dfuse_ctx* ctx = kf->ctx;
+  const long P = kf->P;
+  DF_CUDA(cudaMemcpyAsync(kf->I0, I0, sizeof(float) * P, cudaMemcpyHostToDevice, ctx->stream));
+  launch_texture_mask(ctx, kf->I0, kf->W, kf->H, texture_threshold, kf->mask);
+  launch_mask_list(ctx, kf->mask, P, kf->list, kf->counters + 1);
+  DF_CUDA(cudaMemcpyAsync(&kf->n_mask, kf->counters + 1, sizeof(int), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  reset_state(kf);  // synchronises
+}
+
+void check_kf_args(const dfuse_intrinsics* K, const float* I0, double texture_threshold) {
+  if (!K || !I0) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null pointer"};
+  if (K->width <= 0 || K->height <= 0)
+    throw RefError{DFUSE_E_INVALID_ARGUMENT, "raster dimensions must be positive"};
+  if (texture_threshold <= 0.0)
+    throw RefError{DFUSE_E_INVALID_ARGUMENT, "texture threshold must be > 0"};
+}
+
+// ---- DFPRED ingest (predictions.hpp:31-123) and focal_adjust (148-157) ----
+constexpr size_t kDfpredHeader = 24;
+const char* const kDfpredChannel[6] = {"log_depth",  "log_depth_var", "grad_x",
+                                       "grad_x_var", "grad_y",        "grad_y_var"};
+
+uint32_t rd_u32_le(const unsigned char* p) {
+  return (uint32_t)p[0] | (uint32_t)p[1] << 8 | (uint32_t)p[2] << 16 | (uint32_t)p[3] << 24;
+}
+
+struct DfpredHeader {
+  int w, h;
+  double source_focal;
+};
+
+// load_predictions' header checks, same order, codes and byte offsets
+// (predictions.hpp:72-95)
+DfpredHeader parse_dfpred_header(const unsigned char* b, size_t nbytes) {
+  if (!b) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null buffer"};
+  if (nbytes < kDfpredHeader)
+    throw RefError{DFUSE_E_TRUNCATED_FILE, "dfpred: header, read " + std::to_string(nbytes) +
+                                               " of 24 bytes"};
+  if (memcmp(b, "DFPR", 4) != 0) throw RefError{DFUSE_E_BAD_MAGIC, "dfpred: bad magic at byte 0"};
+  const uint32_t version = rd_u32_le(b + 4);
+  if (version != 1)
+    throw RefError{DFUSE_E_BAD_MAGIC,
+                   "dfpred: unsupported version " + std::to_string(version) + " at byte 4"};
+  const uint32_t width = rd_u32_le(b + 8), height = rd_u32_le(b + 12);
+  const uint32_t channels = rd_u32_le(b + 16), focal_milli = rd_u32_le(b + 20);
+  if (width == 0 || height == 0 || width > 65536 || height > 65536)
+    throw RefError{DFUSE_E_DIMENSION_MISMATCH, "dfpred: " + std::to_string(width) + "x" +
+                                                   std::to_string(height) + " at byte 8"};
+  if (channels != 6)
+    throw RefError{DFUSE_E_DIMENSION_MISMATCH,
+                   "dfpred: channel_count " + std::to_string(channels) + " at byte 16"};
+  if (focal_milli == 0)
+    throw RefError{DFUSE_E_NON_POSITIVE_FOCAL, "dfpred: source_focal at byte 20"};
+  return DfpredHeader{(int)width, (int)height, (double)focal_milli / 1000.0};
+}
+
+// Widen the six fp32 planes to the session's fp64 planes, validate every
+// variance (v > 0 and finite, predictions.hpp:112-118; the first failure in
+// file order wins, as the reference reads channel by channel) and add the
+// focal_adjust shift to log_depth (predictions.hpp:154-155). One thread per
+// (pixel, channel pair), float4-wide reads of the raw planes.
+__global__ void k_dfpred_ingest(const float* __restrict__ raw, long P, double shift, int do_shift,
+                                double* const* __restrict__ planes,
+                                unsigned long long* first_bad) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < P;
+       i += (long)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      double v = (double)raw[(long)c * P + i];
+      if (c & 1) {
+        if (!(v > 0.0 && isfinite(v))) atomicMin(first_bad, (unsigned long long)c * P + i);
+      } else if (c == 0 && do_shift) {
+        v += shift;
+      }
+      planes[c][i] = v;
+    }
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -157,78 +306,15 @@ int dfuse_kf_create(dfuse_ctx* ctx, const dfuse_intrinsics* K, const float* I0,
   if (!kf) return DFUSE_E_CUDA;
   kf->ctx = ctx;
   const int rc = kf_guarded(kf, [&] {
-    if (!K || !I0 || !pred) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null pointer"};
+    check_kf_args(K, I0, texture_threshold);
+    if (!pred) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null pointer"};
     for (int c = 0; c < 6; ++c)
       if (!pred[c]) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null prediction plane"};
-    if (K->width <= 0 || K->height <= 0)
-      throw RefError{DFUSE_E_INVALID_ARGUMENT, "raster dimensions must be positive"};
-    if (texture_threshold <= 0.0)
-      throw RefError{DFUSE_E_INVALID_ARGUMENT, "texture threshold must be > 0"};
-    kf->W = K->width;
-    kf->H = K->height;
-    const long P = kf->P = (long)kf->W * kf->H;
-    kf->grid = fusion_grid(ctx);
-    const size_t dP = al(sizeof(double) * P);
-    const bool resident = fusion_resident_possible(P, kf->grid);
-    const size_t total = 2 * al(sizeof(float) * P) + al(P) + al(sizeof(int) * P) + 2 * dP +
-                         al(P) + 256 + 11 * dP + 11 * dP + al(fusion_slots_bytes(kf->grid)) +
-                         al(sizeof(FusionControl)) + al(2 * sizeof(FusionStateDev)) +
-                         (resident ? al(fusion_halo_bytes(P)) : 0);
-    DF_CUDA(cudaMalloc(&kf->block, total));
-    char* p = (char*)kf->block;
-    auto take = [&](size_t bytes) {
-      char* r = p;
-      p += al(bytes);
-      return (void*)r;
-    };
-    kf->I0 = (float*)take(sizeof(float) * P);
-    kf->I1 = (float*)take(sizeof(float) * P);
-    kf->mask = (uint8_t*)take(P);
-    kf->list = (int*)take(sizeof(int) * P);
-    kf->semi_d = (double*)take(dP);
-    kf->semi_v = (double*)take(dP);
-    kf->semi_valid = (uint8_t*)take(P);
-    kf->counters = (int*)take(256);
-    FusionArgs& f = kf->fa;
-    memset(&f, 0, sizeof f);
-    f.W = kf->W;
-    f.H = kf->H;
-    for (int c = 0; c < 6; ++c) f.pred[c] = (double*)take(dP);
-    f.sd = kf->semi_d;
-    f.sv = kf->semi_v;
-    f.svalid = kf->semi_valid;
-    f.lnsd = (double*)take(dP);
-    f.irs = (double*)take(dP);
-    for (int k = 0; k < 3; ++k) f.ivar[k] = (double*)take(dP);
-    f.inlier_dev = kf->counters + 4;
-    f.ld[0] = (double*)take(dP);
-    f.ld[1] = (double*)take(dP);
-    f.diag = (double*)take(dP);
-    f.right = (double*)take(dP);
-    f.down = (double*)take(dP);
-    f.b = (double*)take(dP);
-    f.x = (double*)take(dP);
-    f.r = (double*)take(dP);
-    f.p[0] = (double*)take(dP);
-    f.p[1] = (double*)take(dP);
-    f.q = (double*)take(dP);
-    f.slots = (ReduceSlot*)take(fusion_slots_bytes(kf->grid));
-    f.halo = resident ? (unsigned long long*)take(fusion_halo_bytes(P)) : nullptr;
-    f.ctl = (FusionControl*)take(sizeof(FusionControl));
-    kf->st = (FusionStateDev*)take(2 * sizeof(FusionStateDev));
-    DF_CUDA(cudaMallocHost(&kf->h_ctl, sizeof(FusionControl)));
-    DF_CUDA(cudaMallocHost(&kf->h_counters, 8 * sizeof(int)));
-    DF_CUDA(cudaMemsetAsync(kf->counters, 0, 256, ctx->stream));
-    DF_CUDA(cudaMemcpyAsync(kf->I0, I0, sizeof(float) * P, cudaMemcpyHostToDevice, ctx->stream));
+    kf_alloc(kf, K);
     for (int c = 0; c < 6; ++c)
-      DF_CUDA(cudaMemcpyAsync((void*)f.pred[c], pred[c], sizeof(double) * P,
+      DF_CUDA(cudaMemcpyAsync((void*)kf->fa.pred[c], pred[c], sizeof(double) * kf->P,
                               cudaMemcpyHostToDevice, ctx->stream));
-    // make_keyframe: texture_mask (pipeline.hpp:148) + the masked-pixel list
-    launch_texture_mask(ctx, kf->I0, kf->W, kf->H, texture_threshold, kf->mask);
-    launch_mask_list(ctx, kf->mask, P, kf->list, kf->counters + 1);
-    DF_CUDA(cudaMemcpyAsync(&kf->n_mask, kf->counters + 1, sizeof(int), cudaMemcpyDeviceToHost,
-                            ctx->stream));
-    reset_state(kf);  // synchronises
+    kf_finish(kf, I0, texture_threshold);
   });
   if (rc) {
     dfuse_kf_destroy(kf);
@@ -236,6 +322,116 @@ int dfuse_kf_create(dfuse_ctx* ctx, const dfuse_intrinsics* K, const float* I0,
   }
   *out = kf;
   return DFUSE_OK;
+}
+
+int dfuse_dfpred_header(dfuse_ctx* ctx, const void* bytes, size_t nbytes, int32_t* width,
+                        int32_t* height, double* source_focal) {
+  try {
+    const DfpredHeader h = parse_dfpred_header((const unsigned char*)bytes, nbytes);
+    if (width) *width = h.w;
+    if (height) *height = h.h;
+    if (source_focal) *source_focal = h.source_focal;
+    if (ctx) ctx->last_error.clear();
+    return DFUSE_OK;
+  } catch (const RefError& e) {
+    if (ctx) ctx->last_error = e.msg;
+    return e.code;
+  }
+}
+
+int dfuse_kf_create_dfpred(dfuse_ctx* ctx, const dfuse_intrinsics* K, const float* I0,
+                           const void* dfpred, size_t nbytes, double texture_threshold,
+                           dfuse_keyframe** out) {
+  if (!ctx || !out) return DFUSE_E_INVALID_ARGUMENT;
+  *out = nullptr;
+  dfuse_keyframe* kf = new (std::nothrow) dfuse_keyframe();
+  if (!kf) return DFUSE_E_CUDA;
+  kf->ctx = ctx;
+  const int rc = kf_guarded(kf, [&] {
+    check_kf_args(K, I0, texture_threshold);
+    const unsigned char* b = (const unsigned char*)dfpred;
+    const DfpredHeader h = parse_dfpred_header(b, nbytes);  // predictions.hpp:72-95
+    const long P = (long)h.w * h.h;
+    const size_t need = kDfpredHeader + 24 * (size_t)P;
+    if (nbytes < need) {  // predictions.hpp:103-108: the first short channel
+      const size_t c = (nbytes - kDfpredHeader) / (4 * (size_t)P);
+      throw RefError{DFUSE_E_TRUNCATED_FILE, std::string("dfpred: channel ") +
+                                                 kDfpredChannel[c] + ", at byte " +
+                                                 std::to_string(nbytes)};
+    }
+    if (h.w != K->width || h.h != K->height)  // pipeline.hpp:139-141
+      throw RefError{DFUSE_E_DIMENSION_MISMATCH,
+                     "dfpred does not match the processing resolution"};
+    kf_alloc(kf, K);
+    // the six fp32 planes go to HBM as they are (24 B/px) and are widened
+    // there; the staging buffer is the fusion workspace's PCG vectors
+    float* raw = (float*)kf->fa.x;  // x, r, p0, p1, q: 5 x 8P >= 24P bytes, contiguous
+    DF_CUDA(cudaMemcpyAsync(raw, b + kDfpredHeader, 24 * (size_t)P, cudaMemcpyHostToDevice,
+                            ctx->stream));
+    const double test_focal = K->fx;  // focal_adjust(pred, camera.fx), pipeline.hpp:145
+    const bool shift_on = test_focal > 0.0 && test_focal != h.source_focal;
+    const double shift = shift_on ? log(test_focal / h.source_focal) : 0.0;
+    double** planes = (double**)scratch(ctx, S_TMP3, sizeof(double*) * 6 + 64);
+    unsigned long long* bad = (unsigned long long*)(planes + 6);
+    double* hp[6];
+    for (int c = 0; c < 6; ++c) hp[c] = (double*)kf->fa.pred[c];
+    const unsigned long long none = ~0ULL;
+    DF_CUDA(cudaMemcpyAsync(planes, hp, sizeof hp, cudaMemcpyHostToDevice, ctx->stream));
+    DF_CUDA(cudaMemcpyAsync(bad, &none, sizeof none, cudaMemcpyHostToDevice, ctx->stream));
+    long blocks = (P + 255) / 256;
+    if (blocks > 8L * ctx->num_sms) blocks = 8L * ctx->num_sms;
+    k_dfpred_ingest<<<(int)blocks, 256, 0, ctx->stream>>>(raw, P, shift, shift_on ? 1 : 0,
+                                                          planes, bad);
+    DF_LAUNCHED(ctx);
+    unsigned long long first = 0;
+    DF_CUDA(cudaMemcpyAsync(&first, bad, sizeof first, cudaMemcpyDeviceToHost, ctx->stream));
+    DF_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (first != none) {  // predictions.hpp:113-117
+      const size_t c = first / P, i = first % P;
+      throw RefError{DFUSE_E_NON_POSITIVE_VARIANCE,
+                     std::string("dfpred: ") + kDfpredChannel[c] + "[" + std::to_string(i) +
+                         "] at byte " + std::to_string(kDfpredHeader + c * P * 4 + i * 4)};
+    }
+    if (!(test_focal > 0.0))  // focal_adjust, predictions.hpp:149-150
+      throw RefError{DFUSE_E_NON_POSITIVE_FOCAL, "focal_adjust requires positive focal lengths"};
+    kf_finish(kf, I0, texture_threshold);
+  });
+  if (rc) {
+    dfuse_kf_destroy(kf);
+    return rc;
+  }
+  *out = kf;
+  return DFUSE_OK;
+}
+
+// median_predicted_depth (pipeline.hpp:94-99): exp of the element
+// nth_element puts at n/2, i.e. the (n/2)-th smallest log-depth -- an exact
+// device radix sort of the keys, one element read back, exp on the host
+// (the reference's std::exp). Cached per keyframe.
+int dfuse_kf_median_depth(dfuse_keyframe* kf, double* out) {
+  return kf_guarded(kf, [&] {
+    if (!out) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null pointer"};
+    if (kf->median_depth < 0.0) {
+      dfuse_ctx* ctx = kf->ctx;
+      const long P = kf->P;
+      // keys in / out: the fusion workspace's r and p0 vectors (idle between frames)
+      const double* keys_in = kf->fa.pred[0];
+      double* keys_out = kf->fa.r;
+      size_t temp = 0;
+      DF_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, temp, keys_in, keys_out, (int)P, 0, 64,
+                                             ctx->stream));
+      void* tmp = scratch(ctx, S_TMP4, temp);
+      DF_CUDA(cub::DeviceRadixSort::SortKeys(tmp, temp, keys_in, keys_out, (int)P, 0, 64,
+                                             ctx->stream));
+      DF_LAUNCHED(ctx);
+      double mid = 0.0;
+      DF_CUDA(cudaMemcpyAsync(&mid, keys_out + P / 2, sizeof mid, cudaMemcpyDeviceToHost,
+                              ctx->stream));
+      DF_CUDA(cudaStreamSynchronize(ctx->stream));
+      kf->median_depth = exp(mid);
+    }
+    *out = kf->median_depth;
+  });
 }
 
 int dfuse_kf_destroy(dfuse_keyframe* kf) {
@@ -297,6 +493,42 @@ int dfuse_kf_download(dfuse_keyframe* kf, double* log_depth, double* scale, int3
     DF_CUDA(cudaStreamSynchronize(ctx->stream));
     if (scale) *scale = st.scale;
     if (iteration) *iteration = st.iteration;
+  });
+}
+
+int dfuse_kf_score(dfuse_keyframe* kf, const double* gt_metres, const uint8_t* gt_valid,
+                   dfuse_keyframe_score* out) {
+  return kf_guarded(kf, [&] {
+    if (!gt_metres || !gt_valid || !out) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null pointer"};
+    dfuse_ctx* ctx = kf->ctx;
+    const long P = kf->P;
+    FusionStateDev st;
+    DF_CUDA(cudaMemcpyAsync(&st, kf->st + kf->parity, sizeof st, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    // ground truth into the idle PCG vectors (q, b) of the fusion workspace
+    double* d_gt = kf->fa.q;
+    uint8_t* d_gv = (uint8_t*)kf->fa.b;
+    DF_CUDA(cudaMemcpyAsync(d_gt, gt_metres, sizeof(double) * P, cudaMemcpyHostToDevice,
+                            ctx->stream));
+    DF_CUDA(cudaMemcpyAsync(d_gv, gt_valid, P, cudaMemcpyHostToDevice, ctx->stream));
+    DF_CUDA(cudaStreamSynchronize(ctx->stream));
+    score_device(ctx, P, nullptr, kf->fa.ld[st.cur], nullptr, d_gt, d_gv, out);
+  });
+}
+
+int dfuse_kf_export_depth_u16(dfuse_keyframe* kf, double depth_scale, uint16_t* out) {
+  return kf_guarded(kf, [&] {
+    if (!out) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null pointer"};
+    dfuse_ctx* ctx = kf->ctx;
+    FusionStateDev st;
+    DF_CUDA(cudaMemcpyAsync(&st, kf->st + kf->parity, sizeof st, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    DF_CUDA(cudaStreamSynchronize(ctx->stream));
+    uint16_t* d = (uint16_t*)kf->fa.q;
+    export_u16_device(ctx, kf->P, kf->fa.ld[st.cur], depth_scale, d);
+    DF_CUDA(cudaMemcpyAsync(out, d, sizeof(uint16_t) * kf->P, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    DF_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 

@@ -422,3 +422,16 @@ def strong_pixel(img: np.ndarray):
         if m[k] > best:
             best, out = float(m[k]), (float(20 + k), float(y))
     return out
+
+
+def to_dfpred(pred: PredictionSet, source_focal: float) -> bytes:
+    """The bytes save_predictions writes (predictions.hpp:125-145): 24-byte
+    little-endian header {"DFPR", version 1, width, height, 6 channels,
+    lround(focal * 1000)} and the six planes as float32 in channel order."""
+    import struct
+    h, w = pred.log_depth.shape
+    focal_milli = int(math.floor(source_focal * 1000.0 + 0.5))  # std::lround for positives
+    head = b"DFPR" + struct.pack("<5I", 1, w, h, 6, focal_milli)
+    planes = [pred.log_depth, pred.log_depth_var, pred.grad_x, pred.grad_x_var, pred.grad_y,
+              pred.grad_y_var]
+    return head + b"".join(np.ascontiguousarray(p, dtype="<f4").tobytes() for p in planes)

@@ -3,7 +3,10 @@
 // restated against include/dfuse/*.hpp, which forward to the CUDA library.
 // Built and run by tests/test_cpp_dropin.py; exit code = failed checks.
 #include <cmath>
+#include <algorithm>
 #include <cstdio>
+#include <fstream>
+#include <vector>
 #include <random>
 
 #include "dfuse/session.hpp"
@@ -284,6 +287,39 @@ static void session_kats() {  // test_pipeline.cpp:57-73, 92-102
   const auto r2 = kf.process_frame(Pose::identity(), Pose::identity(), I0, SearchConfig{1.0, 4.0},
                                    robust, FusionMode::Full);
   CHECK(r2.observations == 0 && kf.fusion().iteration == 2 * robust.gn_iterations);
+
+  // make_keyframe from a DFPRED file (pipeline.hpp:133-147): written the way
+  // save_predictions does (predictions.hpp:125-145), read back on the device
+  const std::string path = "/tmp/dfuse_dropin_test.dfpred";
+  {
+    std::ofstream out(path, std::ios::binary | std::ios::trunc);
+    const uint32_t head[5] = {1u, (uint32_t)sc.K.width, (uint32_t)sc.K.height, 6u,
+                              (uint32_t)std::lround(sc.K.fx * 1000.0)};
+    out.write("DFPR", 4);
+    out.write(reinterpret_cast<const char*>(head), sizeof head);  // little-endian host
+    const Raster<double>* ch[6] = {&pred.log_depth, &pred.log_depth_var, &pred.grad_x,
+                                   &pred.grad_x_var, &pred.grad_y,       &pred.grad_y_var};
+    std::vector<float> buf(pred.log_depth.size());
+    for (const Raster<double>* c : ch) {
+      for (std::size_t i = 0; i < buf.size(); ++i) buf[i] = static_cast<float>((*c)[i]);
+      out.write(reinterpret_cast<const char*>(buf.data()), buf.size() * 4);
+    }
+  }
+  DeviceKeyframe kd(sc.K, I0, path, 0.02);
+  CHECK(kd.fusion().log_depth == pred.log_depth);
+  std::vector<double> v(pred.log_depth.data(), pred.log_depth.data() + pred.log_depth.size());
+  std::nth_element(v.begin(), v.begin() + v.size() / 2, v.end());
+  CHECK(kd.median_depth() == std::exp(v[v.size() / 2]));
+  // retirement (semidense.hpp:419-424): a fresh keyframe has no inliers
+  CHECK(kd.should_create_keyframe(Pose::identity(), Pose::identity()));
+  CHECK(!kd.should_create_keyframe(Pose::identity(), Pose::identity(), KeyframePolicy{0.07, 0}));
+  bool threw = false;
+  try {
+    DeviceKeyframe missing(sc.K, I0, std::string("/nonexistent/x.dfpred"), 0.02);
+  } catch (const Error& e) {
+    threw = e.code() == Err::MissingFile;
+  }
+  CHECK(threw);
 }
 
 int main() {
