@@ -280,6 +280,31 @@ int dfuse_dfpred_header(dfuse_ctx* ctx, const void* bytes, size_t nbytes, int32_
 int dfuse_kf_median_depth(dfuse_keyframe* kf, double* median_depth);
 int dfuse_kf_destroy(dfuse_keyframe* kf);
 
+/* ---- row-band keyframe ------------------------ */
+/* The keyframe split into `bands` row bands, each with its own planes and
+ * one halo row on each side; the stereo stage runs per band, and optimize
+ * runs over all bands with halo-row exchange and a two-level all-reduce
+ * (band level, then across bands). Here every band lives on this context's
+ * device and one cooperative launch runs them all: the single-GPU form of
+ * the multi-GPU layout. Same semantics as dfuse_kf_* (make_keyframe /
+ * process_frame / download), results within the fusion tolerance of the
+ * single-band solve; bands in [1, min(height, SMs)]. */
+typedef struct dfuse_banded_keyframe dfuse_banded_keyframe;
+int dfuse_bkf_create(dfuse_ctx* ctx, const dfuse_intrinsics* K, const float* I0,
+                     const double* const pred[6], double texture_threshold, int bands,
+                     dfuse_banded_keyframe** out);
+int dfuse_bkf_destroy(dfuse_banded_keyframe* kf);
+int dfuse_bkf_reset(dfuse_banded_keyframe* kf);
+int dfuse_bkf_process_frame(dfuse_banded_keyframe* kf, const dfuse_epigeom* g, const float* I1,
+                            const dfuse_search_cfg* scfg, const dfuse_robust_cfg* rcfg, int mode,
+                            dfuse_frame_result* res);
+int dfuse_bkf_process_frame_dev(dfuse_banded_keyframe* kf, const dfuse_epigeom* g,
+                                const float* I1_dev, const dfuse_search_cfg* scfg,
+                                const dfuse_robust_cfg* rcfg, int mode, dfuse_frame_result* res);
+int dfuse_bkf_download(dfuse_banded_keyframe* kf, double* log_depth, double* scale,
+                       int32_t* iteration, double* semi_depth, double* semi_variance,
+                       uint8_t* semi_valid, int32_t* inlier_count, uint8_t* mask);
+
 /* ---- scoring (eval.hpp:34-68, 221-226; pipeline.hpp:232-247) --------- */
 typedef struct {
   double pct_within_10;   /* KeyframeScore::pct_correct */

@@ -63,6 +63,16 @@ def lib() -> C.CDLL:
                                           C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                           C.POINTER(C.c_double)]
         L.dfuse_kf_median_depth.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+        L.dfuse_bkf_create.argtypes = [C.c_void_p, C.POINTER(Intrinsics), C.c_void_p,
+                                       C.POINTER(C.c_void_p), C.c_double, C.c_int,
+                                       C.POINTER(C.c_void_p)]
+        L.dfuse_bkf_destroy.argtypes = [C.c_void_p]
+        L.dfuse_bkf_reset.argtypes = [C.c_void_p]
+        for name in ("dfuse_bkf_process_frame", "dfuse_bkf_process_frame_dev"):
+            f = getattr(L, name)
+            f.argtypes = [C.c_void_p, C.POINTER(EpiGeom), C.c_void_p, C.c_void_p, C.c_void_p,
+                          C.c_int, C.POINTER(FrameResultC)]
+        L.dfuse_bkf_download.argtypes = [C.c_void_p] + [C.c_void_p] * 8
         L.dfuse_score_depth.argtypes = [C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 5
         L.dfuse_kf_score.argtypes = [C.c_void_p] + [C.c_void_p] * 3
         L.dfuse_kf_export_depth_u16.argtypes = [C.c_void_p, C.c_double, C.c_void_p]
@@ -271,3 +281,71 @@ class Keyframe:
             self.close()
         except Exception:
             pass
+
+
+class BandedKeyframe(Keyframe):
+    """A keyframe split into row bands (dfuse_banded_keyframe):
+    the same make_keyframe / process_frame / download as Keyframe, with the
+    per-pixel state in per-band allocations that exchange halo rows and
+    all-reduce through two levels, as across GPUs."""
+
+    _P = "dfuse_bkf_"
+
+    def __init__(self, ctx: Context, camera, I0, pred: PredictionSet, bands: int,
+                 texture_threshold: float = 0.02):
+        L = lib()
+        self.ctx = ctx
+        self.bands = bands
+        self.W, self.H = camera.width, camera.height
+        self._I0 = _f32(I0)
+        self._planes = pred.planes()
+        arr = (C.c_void_p * 6)(*[p.ctypes.data for p in self._planes])
+        kc = camera.c()
+        h = C.c_void_p()
+        rc = L.dfuse_bkf_create(ctx.handle, C.byref(kc), self._I0.ctypes.data, arr,
+                                float(texture_threshold), int(bands), C.byref(h))
+        if rc != 0:
+            raise DfuseError(rc, L.dfuse_last_error(ctx.handle).decode())
+        self.handle = h
+
+    def reset(self):
+        self._check(lib().dfuse_bkf_reset(self.handle), "dfuse_bkf_reset")
+
+    def process_frame(self, g: EpiGeom, I1, search: SearchConfig | None = None,
+                      robust: RobustConfig | None = None, mode="full", device_ptr=None):
+        search = search or SearchConfig()
+        robust = robust or RobustConfig()
+        sc, rc_ = search.c(), robust.c()
+        res = FrameResultC()
+        L = lib()
+        if device_ptr is not None:
+            rc = L.dfuse_bkf_process_frame_dev(self.handle, C.byref(g), C.c_void_p(device_ptr),
+                                               C.byref(sc), C.byref(rc_), _mode(mode),
+                                               C.byref(res))
+        else:
+            img = _f32(I1)
+            rc = L.dfuse_bkf_process_frame(self.handle, C.byref(g), img.ctypes.data,
+                                           C.byref(sc), C.byref(rc_), _mode(mode), C.byref(res))
+        self._check(rc, "dfuse_bkf_process_frame")
+        return res
+
+    def download(self):
+        h, w = self.H, self.W
+        ld = np.zeros((h, w))
+        sd, sv = np.zeros((h, w)), np.zeros((h, w))
+        valid = np.zeros((h, w), np.uint8)
+        mask = np.zeros((h, w), np.uint8)
+        scale = C.c_double(0)
+        it = C.c_int32(0)
+        cnt = C.c_int32(0)
+        self._check(lib().dfuse_bkf_download(self.handle, ld.ctypes.data, C.addressof(scale),
+                                             C.addressof(it), sd.ctypes.data, sv.ctypes.data,
+                                             valid.ctypes.data, C.addressof(cnt),
+                                             mask.ctypes.data), "dfuse_bkf_download")
+        return (FusionState(ld, scale.value, it.value), SemiDenseMap(sd, sv, valid, cnt.value),
+                mask)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().dfuse_bkf_destroy(self.handle)
+            self.handle = None

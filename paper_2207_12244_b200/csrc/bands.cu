@@ -1,0 +1,440 @@
+// bands.cu -- a keyframe split into row bands.
+//
+// Band g owns rows [y0_g, y1_g) of the raster. Everything per pixel that the
+// fusion optimiser keeps (predictions, semi-dense map, log-depth buffers,
+// normal equations, PCG vectors) lives in the band's own allocation, which
+// covers rows [y0 - 1, y1 + 1): one halo row on each side. Plane pointers are
+// shifted so that global pixel indices address them, so the sweeps of
+// fusion.cu run unchanged on a band; the planes read at i - W or i + W get
+// their halo rows from the neighbour band (halo_put / BandNb), and the
+// all-reduces are two-level (BandCtx). The stereo stage needs no exchange:
+// each band scans its own masked pixels against the full I0 / I1 and updates
+// its own semi-dense rows; the inlier count is one shared counter.
+//
+// On one GPU all bands run in one cooperative launch (this file); the
+// multi-GPU layout is the same allocations on different devices, with the
+// BandNb pointers and level-2 arrays mapped from the peers.
+#include <string.h>
+
+#include <new>
+#include <vector>
+
+#include "common.cuh"
+#include "fusion.cuh"
+#include "stereo.cuh"
+
+using namespace dfuse_cuda;
+
+namespace {
+
+size_t al(size_t v) { return (v + 255) & ~size_t(255); }
+
+struct Band {
+  int y0 = 0, y1 = 0;
+  void* block = nullptr;
+  int* list = nullptr;
+  int* counters = nullptr;  // [0] work counter, [1] list length
+  int n_mask = 0;
+  double *semi_d = nullptr, *semi_v = nullptr;
+  uint8_t* semi_valid = nullptr;
+  unsigned long long* rank_slots = nullptr;
+  FusionStateDev* st = nullptr;  // [2]
+  BandNb* nb_dev = nullptr;
+  FusionArgs fa;  // device pointers, shifted to global pixel indices
+  double* plane_base[24];  // unshifted plane starts (for copies)
+};
+
+}  // namespace
+
+struct dfuse_banded_keyframe {
+  dfuse_ctx* ctx = nullptr;
+  int W = 0, H = 0, nband = 0, cpr = 0;
+  long P = 0;
+  void* common = nullptr;  // I0, I1, mask, shared counters, device arg arrays
+  float* I0 = nullptr;
+  float* I1 = nullptr;
+  uint8_t* mask = nullptr;
+  int* shared = nullptr;  // [0] n_obs, [1] inlier_count
+  FusionArgs* d_args = nullptr;
+  unsigned long long** d_rank = nullptr;
+  std::vector<Band> bands;
+  int parity = 0;
+  int stereo_frames = 0;
+  FusionControl* h_ctl = nullptr;  // pinned
+  int* h_shared = nullptr;         // pinned
+};
+
+namespace {
+
+template <class F>
+int bkf_guarded(dfuse_banded_keyframe* kf, F&& f) {
+  if (!kf || !kf->ctx) return DFUSE_E_INVALID_ARGUMENT;
+  dfuse_ctx* ctx = kf->ctx;
+  try {
+    DF_CUDA(cudaSetDevice(ctx->device));
+    f();
+    ctx->last_error.clear();
+    return DFUSE_OK;
+  } catch (const RefError& e) {
+    ctx->last_error = e.msg;
+    return e.code;
+  } catch (const CudaFailure& e) {
+    ctx->last_error = std::string("CUDA: ") + cudaGetErrorString(e.err) + " in " + e.what;
+    return DFUSE_E_CUDA;
+  }
+}
+
+// the band's rows, with halo rows clamped to the image
+inline int lo_row(const Band& b) { return b.y0 > 0 ? b.y0 - 1 : 0; }
+inline int hi_row(const Band& b, int H) { return b.y1 < H ? b.y1 + 1 : H; }
+
+enum BandPlane {  // the 24 double planes of a band, in allocation order
+  BP_PRED0 = 0, BP_SD = 6, BP_SV, BP_LNSD, BP_IRS, BP_IV0, BP_IV1, BP_IV2, BP_LD0, BP_LD1,
+  BP_DIAG, BP_RIGHT, BP_DOWN, BP_B, BP_X, BP_R, BP_P0, BP_P1, BP_Q, BP_COUNT
+};
+static_assert(BP_COUNT == 24, "plane count");
+
+void alloc_band(dfuse_banded_keyframe* kf, Band& b) {
+  const int W = kf->W;
+  const long rows = b.y1 - b.y0 + 2;  // halo row on both sides (unused outside the image)
+  const long n = rows * W;
+  const size_t dP = al(sizeof(double) * n);
+  const size_t total = BP_COUNT * dP + al(n) + al(sizeof(int) * (size_t)(b.y1 - b.y0) * W) + 256 +
+                       al(fusion_slots_bytes(kf->cpr)) + al(band_rank_slots_bytes(kf->nband)) +
+                       al(sizeof(FusionControl)) + al(2 * sizeof(FusionStateDev)) +
+                       al(sizeof(BandNb));
+  DF_CUDA(cudaMalloc(&b.block, total));
+  char* p = (char*)b.block;
+  auto take = [&](size_t bytes) {
+    char* r = p;
+    p += al(bytes);
+    return (void*)r;
+  };
+  const long shift = (long)(b.y0 - 1) * W;  // plane + shift addresses row y0 - 1 at index 0
+  double* sh[BP_COUNT];
+  for (int k = 0; k < BP_COUNT; ++k) {
+    b.plane_base[k] = (double*)take(sizeof(double) * n);
+    sh[k] = b.plane_base[k] - shift;
+  }
+  uint8_t* valid = (uint8_t*)take(n);
+  b.semi_valid = valid - shift;
+  b.list = (int*)take(sizeof(int) * (size_t)(b.y1 - b.y0) * W);
+  b.counters = (int*)take(256);
+  FusionArgs& f = b.fa;
+  memset(&f, 0, sizeof f);
+  f.W = kf->W;
+  f.H = kf->H;
+  for (int c = 0; c < 6; ++c) f.pred[c] = sh[BP_PRED0 + c];
+  b.semi_d = sh[BP_SD];
+  b.semi_v = sh[BP_SV];
+  f.sd = b.semi_d;
+  f.sv = b.semi_v;
+  f.svalid = b.semi_valid;
+  f.lnsd = sh[BP_LNSD];
+  f.irs = sh[BP_IRS];
+  for (int k = 0; k < 3; ++k) f.ivar[k] = sh[BP_IV0 + k];
+  f.ld[0] = sh[BP_LD0];
+  f.ld[1] = sh[BP_LD1];
+  f.diag = sh[BP_DIAG];
+  f.right = sh[BP_RIGHT];
+  f.down = sh[BP_DOWN];
+  f.b = sh[BP_B];
+  f.x = sh[BP_X];
+  f.r = sh[BP_R];
+  f.p[0] = sh[BP_P0];
+  f.p[1] = sh[BP_P1];
+  f.q = sh[BP_Q];
+  f.slots = (ReduceSlot*)take(fusion_slots_bytes(kf->cpr));
+  b.rank_slots = (unsigned long long*)take(band_rank_slots_bytes(kf->nband));
+  f.ctl = (FusionControl*)take(sizeof(FusionControl));
+  b.st = (FusionStateDev*)take(2 * sizeof(FusionStateDev));
+  b.nb_dev = (BandNb*)take(sizeof(BandNb));
+  f.inlier_dev = kf->shared + 1;
+  f.band_y0 = b.y0;
+  f.band_y1 = b.y1;
+  f.band_ctas = kf->cpr;
+  f.nb = b.nb_dev;
+  DF_CUDA(cudaMemsetAsync(b.counters, 0, 256, kf->ctx->stream));
+}
+
+// BandNb of band g: the halo planes of its neighbours (HaloPlane order)
+BandNb neighbours(dfuse_banded_keyframe* kf, int g) {
+  BandNb nb;
+  memset(&nb, 0, sizeof nb);
+  auto planes = [](const FusionArgs& f, double** out) {
+    out[HP_LD0] = f.ld[0];
+    out[HP_LD1] = f.ld[1];
+    out[HP_X] = f.x;
+    out[HP_R] = f.r;
+    out[HP_DIAG] = f.diag;
+    out[HP_DOWN] = f.down;
+    out[HP_P0] = f.p[0];
+    out[HP_P1] = f.p[1];
+    out[HP_IV2] = f.ivar[2];
+  };
+  if (g > 0) planes(kf->bands[g - 1].fa, nb.up);
+  if (g + 1 < kf->nband) planes(kf->bands[g + 1].fa, nb.dn);
+  return nb;
+}
+
+void reset_bkf(dfuse_banded_keyframe* kf) {
+  dfuse_ctx* ctx = kf->ctx;
+  const int W = kf->W;
+  for (Band& b : kf->bands) {
+    const long n = (long)(b.y1 - b.y0 + 2) * W;
+    DF_CUDA(cudaMemsetAsync(b.plane_base[BP_SD], 0, sizeof(double) * n, ctx->stream));
+    DF_CUDA(cudaMemsetAsync(b.plane_base[BP_SV], 0, sizeof(double) * n, ctx->stream));
+    DF_CUDA(cudaMemsetAsync(b.semi_valid + (long)(b.y0 - 1) * W, 0, n, ctx->stream));
+    // init_state (fusion.hpp:44-46), halo rows included: they hold the
+    // neighbours' rows of the same raster
+    DF_CUDA(cudaMemcpyAsync(b.plane_base[BP_LD0], b.plane_base[BP_PRED0], sizeof(double) * n,
+                            cudaMemcpyDeviceToDevice, ctx->stream));
+    FusionStateDev s0{1.0, 0, 0};
+    DF_CUDA(cudaMemcpyAsync(b.st, &s0, sizeof s0, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  DF_CUDA(cudaMemsetAsync(kf->shared, 0, 2 * sizeof(int), ctx->stream));
+  DF_CUDA(cudaStreamSynchronize(ctx->stream));
+  kf->parity = 0;
+  kf->stereo_frames = 0;
+}
+
+void process_bkf(dfuse_banded_keyframe* kf, const dfuse_epigeom* g, const float* I1_dev,
+                 const dfuse_search_cfg* scfg, const dfuse_robust_cfg* rcfg, int mode,
+                 dfuse_frame_result* res) {
+  dfuse_ctx* ctx = kf->ctx;
+  if (!g || !scfg || !rcfg || !res) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null pointer"};
+  if (g->K.width != kf->W || g->K.height != kf->H)
+    throw RefError{DFUSE_E_DIMENSION_MISMATCH, "frame does not match the keyframe raster"};
+  if (mode < 0 || mode > 2) throw RefError{DFUSE_E_INVALID_ARGUMENT, "unknown fusion mode"};
+  if (rcfg->gn_iterations > 0) {
+    const bool ls = mode == DFUSE_MODE_LSSCALE;
+    if (rcfg->delta_semi <= 0.0 || (!ls && rcfg->delta_net <= 0.0) ||
+        (mode != DFUSE_MODE_NOPAIRWISE && rcfg->delta_grad <= 0.0))
+      throw RefError{DFUSE_E_INVALID_ARGUMENT, "huber delta must be > 0"};
+  }
+  // stereo stage: every band scans its own masked pixels (pipeline.hpp:205-213)
+  DF_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+  DF_CUDA(cudaMemsetAsync(kf->shared, 0, sizeof(int), ctx->stream));  // n_obs
+  for (Band& b : kf->bands) {
+    if (b.n_mask == 0) continue;
+    StereoArgs a;
+    memset(&a, 0, sizeof a);
+    a.g = *g;
+    a.cfg = *scfg;
+    a.I0 = kf->I0;
+    a.I1 = I1_dev;
+    a.n_items = b.n_mask;
+    a.work_counter = b.counters;
+    a.list = b.list;
+    a.depth = b.semi_d;
+    a.variance = b.semi_v;
+    a.valid = b.semi_valid;
+    a.n_obs = kf->shared;
+    a.n_installed = kf->shared + 1;
+    launch_stereo(ctx, a, false);
+  }
+  DF_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+  // optimise stage over all bands (pipeline.hpp:223-226)
+  std::vector<FusionArgs> args(kf->nband);
+  for (int k = 0; k < kf->nband; ++k) {
+    Band& b = kf->bands[k];
+    FusionArgs f = b.fa;
+    f.dsemi = rcfg->delta_semi;
+    f.dnet = rcfg->delta_net;
+    f.dgrad = rcfg->delta_grad;
+    f.cg_tol = rcfg->cg_tol;
+    f.gn = rcfg->gn_iterations;
+    f.cg_max = rcfg->cg_max_iters;
+    f.est_scale = rcfg->estimate_scale;
+    f.mode = mode;
+    f.op = OP_OPTIMIZE;
+    f.st_in = b.st + kf->parity;
+    f.st_out = b.st + (1 - kf->parity);
+    f.band_cta0 = k * kf->cpr;
+    args[k] = f;
+    // LL flags restart at 1 every launch
+    DF_CUDA(cudaMemsetAsync(f.slots, 0, fusion_slots_bytes(kf->cpr), ctx->stream));
+    DF_CUDA(cudaMemsetAsync(b.rank_slots, 0, band_rank_slots_bytes(kf->nband), ctx->stream));
+  }
+  DF_CUDA(cudaMemcpyAsync(kf->d_args, args.data(), sizeof(FusionArgs) * kf->nband,
+                          cudaMemcpyHostToDevice, ctx->stream));
+  launch_fusion_banded(ctx, kf->d_args, kf->d_rank, kf->nband, kf->cpr);
+  DF_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
+  DF_CUDA(cudaMemcpyAsync(kf->h_shared, kf->shared, 2 * sizeof(int), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  DF_CUDA(cudaMemcpyAsync(kf->h_ctl, kf->bands[0].fa.ctl, sizeof(FusionControl),
+                          cudaMemcpyDeviceToHost, ctx->stream));
+  DF_CUDA(cudaStreamSynchronize(ctx->stream));
+  kf->parity = 1 - kf->parity;
+  const int n_obs = kf->h_shared[0];
+  if (n_obs > 0) kf->stereo_frames += 1;  // pipeline.hpp:211
+  res->observations = n_obs;
+  res->inlier_count = kf->h_shared[1];
+  res->stereo_frames = kf->stereo_frames;
+  res->optimize_status = kf->h_ctl->status;
+  DF_CUDA(cudaEventElapsedTime(&res->stereo_ms, ctx->ev[0], ctx->ev[1]));
+  DF_CUDA(cudaEventElapsedTime(&res->optimise_ms, ctx->ev[1], ctx->ev[2]));
+  res->stats = kf->h_ctl->stats;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dfuse_bkf_destroy(dfuse_banded_keyframe* kf) {
+  if (!kf) return DFUSE_OK;
+  if (kf->ctx) {
+    cudaSetDevice(kf->ctx->device);
+    cudaStreamSynchronize(kf->ctx->stream);
+  }
+  for (Band& b : kf->bands)
+    if (b.block) cudaFree(b.block);
+  if (kf->common) cudaFree(kf->common);
+  if (kf->h_ctl) cudaFreeHost(kf->h_ctl);
+  if (kf->h_shared) cudaFreeHost(kf->h_shared);
+  delete kf;
+  return DFUSE_OK;
+}
+
+int dfuse_bkf_create(dfuse_ctx* ctx, const dfuse_intrinsics* K, const float* I0,
+                     const double* const pred[6], double texture_threshold, int bands,
+                     dfuse_banded_keyframe** out) {
+  if (!ctx || !out) return DFUSE_E_INVALID_ARGUMENT;
+  *out = nullptr;
+  dfuse_banded_keyframe* kf = new (std::nothrow) dfuse_banded_keyframe();
+  if (!kf) return DFUSE_E_CUDA;
+  kf->ctx = ctx;
+  const int rc = bkf_guarded(kf, [&] {
+    if (!K || !I0 || !pred) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null pointer"};
+    for (int c = 0; c < 6; ++c)
+      if (!pred[c]) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null prediction plane"};
+    if (K->width <= 0 || K->height <= 0)
+      throw RefError{DFUSE_E_INVALID_ARGUMENT, "raster dimensions must be positive"};
+    if (texture_threshold <= 0.0)
+      throw RefError{DFUSE_E_INVALID_ARGUMENT, "texture threshold must be > 0"};
+    if (bands < 1 || bands > K->height || bands > ctx->num_sms)
+      throw RefError{DFUSE_E_INVALID_ARGUMENT, "bands must be in [1, min(height, SMs)]"};
+    kf->W = K->width;
+    kf->H = K->height;
+    kf->P = (long)kf->W * kf->H;
+    kf->nband = bands;
+    kf->cpr = fusion_grid(ctx) / bands;  // CTAs per band (one per SM overall)
+    const long P = kf->P;
+    const size_t common = 2 * al(sizeof(float) * P) + al(P) + 256 +
+                          al(sizeof(FusionArgs) * bands) + al(sizeof(void*) * bands);
+    DF_CUDA(cudaMalloc(&kf->common, common));
+    char* p = (char*)kf->common;
+    auto take = [&](size_t bytes) {
+      char* r = p;
+      p += al(bytes);
+      return (void*)r;
+    };
+    kf->I0 = (float*)take(sizeof(float) * P);
+    kf->I1 = (float*)take(sizeof(float) * P);
+    kf->mask = (uint8_t*)take(P);
+    kf->shared = (int*)take(256);
+    kf->d_args = (FusionArgs*)take(sizeof(FusionArgs) * bands);
+    kf->d_rank = (unsigned long long**)take(sizeof(void*) * bands);
+    DF_CUDA(cudaMallocHost(&kf->h_ctl, sizeof(FusionControl)));
+    DF_CUDA(cudaMallocHost(&kf->h_shared, 8 * sizeof(int)));
+    kf->bands.resize(bands);
+    for (int g = 0; g < bands; ++g) {  // even row split
+      kf->bands[g].y0 = (int)((long)kf->H * g / bands);
+      kf->bands[g].y1 = (int)((long)kf->H * (g + 1) / bands);
+      alloc_band(kf, kf->bands[g]);
+    }
+    std::vector<unsigned long long*> rank(bands);
+    for (int g = 0; g < bands; ++g) {
+      Band& b = kf->bands[g];
+      rank[g] = b.rank_slots;
+      const BandNb nb = neighbours(kf, g);
+      DF_CUDA(cudaMemcpyAsync(b.nb_dev, &nb, sizeof nb, cudaMemcpyHostToDevice, ctx->stream));
+      // predictions: the band's rows and its halo rows (pred[4] is read at i - W)
+      const int r0 = lo_row(b), r1 = hi_row(b, kf->H);
+      for (int c = 0; c < 6; ++c)
+        DF_CUDA(cudaMemcpyAsync((double*)b.fa.pred[c] + (long)r0 * kf->W,
+                                pred[c] + (long)r0 * kf->W,
+                                sizeof(double) * (size_t)(r1 - r0) * kf->W,
+                                cudaMemcpyHostToDevice, ctx->stream));
+    }
+    DF_CUDA(cudaMemcpyAsync(kf->d_rank, rank.data(), sizeof(void*) * bands,
+                            cudaMemcpyHostToDevice, ctx->stream));
+    DF_CUDA(cudaMemcpyAsync(kf->I0, I0, sizeof(float) * P, cudaMemcpyHostToDevice, ctx->stream));
+    // make_keyframe: texture_mask (pipeline.hpp:148), then each band's list
+    launch_texture_mask(ctx, kf->I0, kf->W, kf->H, texture_threshold, kf->mask);
+    for (Band& b : kf->bands) {
+      const long off = (long)b.y0 * kf->W;
+      launch_mask_list(ctx, kf->mask + off, (long)(b.y1 - b.y0) * kf->W, b.list, b.counters + 1,
+                       off);
+      DF_CUDA(cudaMemcpyAsync(&b.n_mask, b.counters + 1, sizeof(int), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    }
+    reset_bkf(kf);  // synchronises
+  });
+  if (rc) {
+    dfuse_bkf_destroy(kf);
+    return rc;
+  }
+  *out = kf;
+  return DFUSE_OK;
+}
+
+int dfuse_bkf_reset(dfuse_banded_keyframe* kf) {
+  return bkf_guarded(kf, [&] { reset_bkf(kf); });
+}
+
+int dfuse_bkf_process_frame(dfuse_banded_keyframe* kf, const dfuse_epigeom* g, const float* I1,
+                            const dfuse_search_cfg* scfg, const dfuse_robust_cfg* rcfg, int mode,
+                            dfuse_frame_result* res) {
+  return bkf_guarded(kf, [&] {
+    if (!I1) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null image"};
+    DF_CUDA(cudaMemcpyAsync(kf->I1, I1, sizeof(float) * kf->P, cudaMemcpyHostToDevice,
+                            kf->ctx->stream));
+    process_bkf(kf, g, kf->I1, scfg, rcfg, mode, res);
+  });
+}
+
+int dfuse_bkf_process_frame_dev(dfuse_banded_keyframe* kf, const dfuse_epigeom* g,
+                                const float* I1_dev, const dfuse_search_cfg* scfg,
+                                const dfuse_robust_cfg* rcfg, int mode,
+                                dfuse_frame_result* res) {
+  return bkf_guarded(kf, [&] {
+    if (!I1_dev) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null image"};
+    process_bkf(kf, g, I1_dev, scfg, rcfg, mode, res);
+  });
+}
+
+int dfuse_bkf_download(dfuse_banded_keyframe* kf, double* log_depth, double* scale,
+                       int32_t* iteration, double* semi_depth, double* semi_variance,
+                       uint8_t* semi_valid, int32_t* inlier_count, uint8_t* mask) {
+  return bkf_guarded(kf, [&] {
+    dfuse_ctx* ctx = kf->ctx;
+    FusionStateDev st;
+    DF_CUDA(cudaMemcpyAsync(&st, kf->bands[0].st + kf->parity, sizeof st,
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    DF_CUDA(cudaStreamSynchronize(ctx->stream));
+    const int W = kf->W;
+    for (const Band& b : kf->bands) {  // each band's own rows
+      const long o = (long)b.y0 * W;
+      const size_t n = (size_t)(b.y1 - b.y0) * W;
+      auto cp = [&](void* dst, const void* src, size_t elem) {
+        if (dst)
+          DF_CUDA(cudaMemcpyAsync((char*)dst + o * elem, (const char*)src + o * elem, n * elem,
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+      };
+      cp(log_depth, b.fa.ld[st.cur], sizeof(double));
+      cp(semi_depth, b.semi_d, sizeof(double));
+      cp(semi_variance, b.semi_v, sizeof(double));
+      cp(semi_valid, b.semi_valid, 1);
+    }
+    if (inlier_count)
+      DF_CUDA(cudaMemcpyAsync(inlier_count, kf->shared + 1, sizeof(int), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    if (mask) DF_CUDA(cudaMemcpyAsync(mask, kf->mask, kf->P, cudaMemcpyDeviceToHost, ctx->stream));
+    DF_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (scale) *scale = st.scale;
+    if (iteration) *iteration = st.iteration;
+  });
+}
+
+}  // extern "C"

@@ -146,6 +146,7 @@ __device__ __forceinline__ double ll_wait(const unsigned long long* p, unsigned 
 // ---------------------------------------------------------------------------
 // grid all-reduce
 struct GridCtx {
+  static constexpr bool kHier = false;
   ReduceSlot* slots;  // LL slot array (fusion_slots_bytes)
   unsigned G;
   unsigned long long base_tag;  // atomic-counter microbenchmark variant only
@@ -153,6 +154,38 @@ struct GridCtx {
   int syncs;
   unsigned ll_next;  // next free LL flag for the resident PCG halo exchange
 };
+
+// Row-band launch: the CTAs of band b form one LL all-reduce
+// group (slots = the band's level-1 array, G = CTAs per band, me = index in
+// the band); the band totals then travel through level-2 LL arrays, one per
+// band, into which every band's leader CTA posts its total (remote stores
+// when bands sit on different GPUs) and which the band's own CTAs poll; each
+// CTA adds the band totals in band order, so every CTA of every band holds
+// the same bits.
+struct BandCtx : GridCtx {
+  static constexpr bool kHier = true;
+  unsigned me, band, nband;
+  unsigned long long* const* rank_slots;  // [nband] level-2 arrays
+  int sys;  // fences at system scope (bands on several GPUs)
+};
+
+template <class Ctx>
+__device__ __forceinline__ unsigned cta_index(const Ctx& c) {
+  if constexpr (Ctx::kHier)
+    return c.me;
+  else
+    return blockIdx.x;
+}
+template <class Ctx>
+__device__ __forceinline__ void ctx_fence(const Ctx& c) {
+  if constexpr (Ctx::kHier) {
+    if (c.sys) {
+      __threadfence_system();
+      return;
+    }
+  }
+  __threadfence();
+}
 
 // LL all-reduce slots: value k of CTA b in phase parity q is one 16-byte
 // {low, high} LL pair at its own 256-byte stride (the L2 hashes 256-byte
@@ -181,15 +214,15 @@ __device__ __forceinline__ void cta_partial(double (&v)[NV], double (&t)[NV], do
 }
 
 // warp 0 posts the CTA's partials: lane k stores value k as one LL pair
-template <int NV>
-__device__ __forceinline__ void ll_publish(const GridCtx& c, const double (&t)[NV]) {
+template <int NV, class Ctx>
+__device__ __forceinline__ void ll_publish(const Ctx& c, const double (&t)[NV]) {
   const int lane = threadIdx.x & 31;
   if (lane < NV) {
     double tk = t[0];
 #pragma unroll
     for (int k = 1; k < NV; ++k)
       if (lane == k) tk = t[k];
-    st_relaxed_v2(ll_slot(c, c.phase, lane, blockIdx.x), ll_word(tk, 0, c.phase + 1),
+    st_relaxed_v2(ll_slot(c, c.phase, lane, cta_index(c)), ll_word(tk, 0, c.phase + 1),
                   ll_word(tk, 1, c.phase + 1));
   }
 }
@@ -205,8 +238,8 @@ __device__ __forceinline__ void ll_publish(const GridCtx& c, const double (&t)[N
 // pol[w][k]; poll_total adds them in warp order (same bits in every CTA).
 constexpr int kPollWarps = 5;
 constexpr int kMaxPollSlots = 2;  // slots per lane: grids up to 32*5*2 = 320 CTAs
-template <int NV, bool FENCE>
-__device__ __forceinline__ void ll_poll(const GridCtx& c, double* pol, long long* rec) {
+template <int NV, bool FENCE, class Ctx>
+__device__ __forceinline__ void ll_poll(const Ctx& c, double* pol, long long* rec) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (wid >= kPollWarps) return;
   const unsigned flag = c.phase + 1;
@@ -231,7 +264,7 @@ __device__ __forceinline__ void ll_poll(const GridCtx& c, double* pol, long long
     if (rec && threadIdx.x == 0) rec[3] += 1;  // diagnostics: poll rounds of warp 0
     if (__all_sync(0xffffffffu, ok)) break;
   }
-  if (FENCE) __threadfence();
+  if (FENCE) ctx_fence(c);
 #pragma unroll
   for (int k = 0; k < NV; ++k) acc[k] = warp_sum(acc[k]);
   if (lane == 0)
@@ -256,8 +289,48 @@ __device__ __forceinline__ void poll_total(const double* pol, double (&v)[NV]) {
 // global read after it, grid-wide (needed whenever other CTAs read data this
 // CTA wrote). VARIANT 10 = LL all-to-all (production); 2 = atomic arrival
 // counter (sync microbenchmark baseline). rec: DFUSE_TRACE=3 timestamps.
-template <int NV, bool FENCE = true, int VARIANT = 10>
-__device__ void grid_allreduce(GridCtx& c, double (&v)[NV], long long* rec = nullptr) {
+// level 2 of a banded all-reduce: v (the band total, identical in every CTA
+// of the band) -> the sum of all band totals in band order
+template <int NV, bool FENCE>
+__device__ void band_exchange(BandCtx& c, double (&v)[NV]) {
+  __shared__ double pol2[4];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (wid == 0) {
+    const unsigned flag = c.phase + 1;
+    auto slot = [&](unsigned h, int k, unsigned src) {
+      return c.rank_slots[h] + (((size_t)(c.phase & 1) * 4 + k) * c.nband + src) * kSlotWords;
+    };
+    if (lane < NV) {
+      double tk = v[0];
+#pragma unroll
+      for (int k = 1; k < NV; ++k)
+        if (lane == k) tk = v[k];
+      if (c.me == 0)  // the band's leader posts the band total to every band
+        for (unsigned h = 0; h < c.nband; ++h)
+          st_relaxed_v2(slot(h, lane, c.band), ll_word(tk, 0, flag), ll_word(tk, 1, flag));
+      double sum;
+      for (;;) {
+        bool ok = true;
+        sum = 0.0;
+        for (unsigned h = 0; h < c.nband; ++h) {
+          unsigned long long w0, w1;
+          ld_relaxed_v2(slot(c.band, lane, h), w0, w1);
+          ok &= (unsigned)(w0 >> 32) == flag && (unsigned)(w1 >> 32) == flag;
+          sum += ll_value(w0, w1);
+        }
+        if (ok) break;
+      }
+      pol2[lane] = sum;
+    }
+    if (FENCE) ctx_fence(c);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = pol2[k];
+}
+
+template <int NV, bool FENCE = true, int VARIANT = 10, class Ctx = GridCtx>
+__device__ void grid_allreduce(Ctx& c, double (&v)[NV], long long* rec = nullptr) {
   __shared__ double red[FW * 4];
   __shared__ double pol[kPollWarps * 4];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -268,7 +341,7 @@ __device__ void grid_allreduce(GridCtx& c, double (&v)[NV], long long* rec = nul
     if (wid == 0) {
       // release: the CTA's earlier global writes (ordered before this point
       // by the barrier in cta_partial) become visible before the LL words
-      if (FENCE) __threadfence();
+      if (FENCE) ctx_fence(c);
       if (rec && lane == 0) rec[1] = clock64();
       ll_publish(c, t);
     }
@@ -276,6 +349,9 @@ __device__ void grid_allreduce(GridCtx& c, double (&v)[NV], long long* rec = nul
     if (rec && threadIdx.x == 0) rec[2] = clock64();
     __syncthreads();
     poll_total(pol, v);
+    if constexpr (Ctx::kHier) {
+      if (c.nband > 1) band_exchange<NV, FENCE>(c, v);
+    }
   } else {
     ReduceSlot* buf = c.slots + (size_t)(c.phase & 1) * c.G;
     if (wid == 0) {
@@ -311,7 +387,8 @@ __device__ void grid_allreduce(GridCtx& c, double (&v)[NV], long long* rec = nul
   c.syncs += 1;
 }
 
-__device__ __forceinline__ void grid_sync(GridCtx& c) {
+template <class Ctx>
+__device__ __forceinline__ void grid_sync(Ctx& c) {
   double none[1] = {0.0};
   grid_allreduce(c, none);
 }
@@ -379,11 +456,30 @@ struct Range {
 };
 
 __device__ __forceinline__ Range my_range(const FusionArgs& a) {
-  const long P = (long)a.W * a.H;
   Range r;
-  r.beg = (int)(P * blockIdx.x / gridDim.x);
-  r.end = (int)(P * (blockIdx.x + 1) / gridDim.x);
+  if (a.band_ctas > 0) {  // the band's rows among the band's CTAs
+    const long b0 = (long)a.band_y0 * a.W, len = (long)(a.band_y1 - a.band_y0) * a.W;
+    const long k = (long)blockIdx.x - a.band_cta0;
+    r.beg = (int)(b0 + len * k / a.band_ctas);
+    r.end = (int)(b0 + len * (k + 1) / a.band_ctas);
+  } else {
+    const long P = (long)a.W * a.H;
+    r.beg = (int)(P * blockIdx.x / gridDim.x);
+    r.end = (int)(P * (blockIdx.x + 1) / gridDim.x);
+  }
   return r;
+}
+
+// the neighbour band's copy of a boundary-row value (no-op unless banded)
+__device__ __forceinline__ void halo_put(const BandNb* nb, int y0, int y1, int plane, int i, int y,
+                                         double v) {
+  if (nb) {
+    if (y == y0 && nb->up[plane]) nb->up[plane][i] = v;
+    if (y == y1 - 1 && nb->dn[plane]) nb->dn[plane][i] = v;
+  }
+}
+__device__ __forceinline__ void halo_put(const FusionArgs& a, int plane, int i, double v) {
+  if (a.nb) halo_put(a.nb, a.band_y0, a.band_y1, plane, i, i / a.W, v);
 }
 
 // ---------------------------------------------------------------------------
@@ -430,6 +526,7 @@ __device__ void sweep_prologue(const FusionArgs& a, const Range& rg) {
     a.ivar[0][i] = 1.0 / a.pred[1][i];
     a.ivar[1][i] = 1.0 / a.pred[3][i];
     a.ivar[2][i] = 1.0 / a.pred[5][i];
+    halo_put(a, HP_IV2, i, a.ivar[2][i]);
   }
 }
 
@@ -463,7 +560,9 @@ __device__ __forceinline__ double sweep_cost_body(const Range rg, const int W, c
                                                   const double dsemi, const double dgrad,
                                                   const double ln_s, const double* __restrict__ ld,
                                                   const double* __restrict__ xs, const double step,
-                                                  const SweepPlanes pl, double* __restrict__ wt) {
+                                                  const SweepPlanes pl, double* __restrict__ wt,
+                                                  const BandNb* nb, const int y0, const int y1,
+                                                  const int wt_plane) {
   double cost = 0.0;
   for (int i0 = rg.beg + threadIdx.x; i0 < rg.end; i0 += U * FT) {
 #pragma unroll
@@ -481,7 +580,10 @@ __device__ __forceinline__ double sweep_cost_body(const Range rg, const int W, c
                                   pl.lns[i], pl.irs[i], pl.p2[i], pl.iv1[i], pl.p4[i], pl.iv2[i],
                                   dnet, dsemi, dgrad, ln_s);
       if (in) {
-        if (wt) wt[i] = li;
+        if (wt) {
+          wt[i] = li;
+          halo_put(nb, y0, y1, wt_plane, i, y, li);
+        }
         cost += c;
       }
     }
@@ -492,12 +594,15 @@ __device__ __forceinline__ double sweep_cost_body(const Range rg, const int W, c
 template <int U, class LD>
 __device__ double sweep_cost(const FusionArgs& a, const Sel& sel, const Range& rg, const LD& L,
                              double ln_s, double* write_trial) {
+  const int wplane = write_trial == a.ld[0] ? HP_LD0 : HP_LD1;
   if constexpr (LD::kTrial)  // trial = st + step * delta (fusion.hpp:432-433)
     return sweep_cost_body<U, true>(rg, a.W, a.H, sel, a.dnet, a.dsemi, a.dgrad, ln_s, L.ld, L.x,
-                                    L.step, planes_of(a), write_trial);
+                                    L.step, planes_of(a), write_trial, a.nb, a.band_y0,
+                                    a.band_y1, wplane);
   else
     return sweep_cost_body<U, false>(rg, a.W, a.H, sel, a.dnet, a.dsemi, a.dgrad, ln_s, L.ld,
-                                     nullptr, 0.0, planes_of(a), write_trial);
+                                     nullptr, 0.0, planes_of(a), write_trial, a.nb, a.band_y0,
+                                     a.band_y1, wplane);
 }
 
 // scale IRLS round (fusion.hpp:379-388) [+ total_cost at ln_s_cost]
@@ -583,7 +688,8 @@ __device__ __forceinline__ void sweep_assemble_body(
     const Range rg, const int W, const int H, const Sel sel, const double dnet, const double dsemi,
     const double dgrad, const double* __restrict__ ld, const double ln_s, const SweepPlanes pl,
     double* __restrict__ o_diag, double* __restrict__ o_right, double* __restrict__ o_down,
-    double* __restrict__ o_r, double* __restrict__ o_b, double (&v)[4]) {
+    double* __restrict__ o_r, double* __restrict__ o_b, double (&v)[4], const BandNb* nb,
+    const int y0, const int y1) {
   double bn = 0.0, rz = 0.0, bad = 0.0, cost = 0.0;
   for (int i0 = rg.beg + threadIdx.x; i0 < rg.end; i0 += U * FT) {
 #pragma unroll
@@ -649,6 +755,9 @@ __device__ __forceinline__ void sweep_assemble_body(
         o_right[i] = right;
         o_down[i] = down;
         o_r[i] = b;
+        halo_put(nb, y0, y1, HP_DIAG, i, y, diag);
+        halo_put(nb, y0, y1, HP_DOWN, i, y, down);
+        halo_put(nb, y0, y1, HP_R, i, y, b);
         if (o_b) o_b[i] = b;
         bn += b * b;
         if (!(diag > 0.0)) bad += 1.0;
@@ -667,7 +776,8 @@ template <int U>
 __device__ void sweep_assemble(const FusionArgs& a, const Sel& sel, const Range& rg,
                                const double* ld, double ln_s, bool store_b, double (&v)[4]) {
   sweep_assemble_body<U>(rg, a.W, a.H, sel, a.dnet, a.dsemi, a.dgrad, ld, ln_s, planes_of(a),
-                         a.diag, a.right, a.down, a.r, store_b ? a.b : nullptr, v);
+                         a.diag, a.right, a.down, a.r, store_b ? a.b : nullptr, v, a.nb,
+                         a.band_y0, a.band_y1);
 }
 
 // standalone PCG init from (diag, right, down, b)
@@ -687,7 +797,10 @@ __device__ void sweep_pcg_init(const FusionArgs& a, const Range& rg, double (&v)
 }
 
 __device__ void sweep_zero_x(const FusionArgs& a, const Range& rg) {
-  for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) a.x[i] = 0.0;
+  for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) {
+    a.x[i] = 0.0;
+    halo_put(a, HP_X, i, 0.0);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -716,6 +829,7 @@ __device__ double sweep_pcg_a(const FusionArgs& a, const Range& rg, int it, doub
     if (y + 1 < H) v += a.down[i] * p_at(a, pprev, beta, first, i + W);
     if (y > 0) v += a.down[i - W] * p_at(a, pprev, beta, first, i - W);
     pcur[i] = pi;
+    halo_put(a, (it & 1) ? HP_P1 : HP_P0, i, pi);
     a.q[i] = v;
     pq += pi * v;
   }
@@ -729,9 +843,12 @@ __device__ void sweep_pcg_b(const FusionArgs& a, const Range& rg, int it, double
   double rr = 0.0, rz = 0.0;
   for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) {
     const double xo = it == 0 ? 0.0 : a.x[i];
-    a.x[i] = xo + alpha * pcur[i];
+    const double xn = xo + alpha * pcur[i];
+    a.x[i] = xn;
+    halo_put(a, HP_X, i, xn);
     const double r = a.r[i] - alpha * a.q[i];
     a.r[i] = r;
+    halo_put(a, HP_R, i, r);
     rr += r * r;
     rz += r * (r / a.diag[i]);
   }
@@ -741,7 +858,8 @@ __device__ void sweep_pcg_b(const FusionArgs& a, const Range& rg, int it, double
 
 // Jacobi PCG after init (solve_depth_step, fusion.hpp:334-367). Returns the
 // error code (0 ok); *its = iterations run.
-__device__ int pcg_stream(GridCtx& c, const FusionArgs& a, const Range& rg, double bnorm2,
+template <class Ctx>
+__device__ int pcg_stream(Ctx& c, const FusionArgs& a, const Range& rg, double bnorm2,
                           double rz, int* its) {
   const double tol2 = a.cg_tol * a.cg_tol * bnorm2;
   double prev = bnorm2;
@@ -793,8 +911,8 @@ __device__ __forceinline__ TileGeo my_tile(const FusionArgs& a) {
 
 #include "pcg_tile.cuh"
 
-template <int PPT, int VAR>
-__device__ __forceinline__ int pcg_solve(GridCtx& c, const FusionArgs& a, const Range& rg,
+template <int PPT, int VAR, class Ctx>
+__device__ __forceinline__ int pcg_solve(Ctx& c, const FusionArgs& a, const Range& rg,
                                          double bnorm2, double rz, int* its) {
   if constexpr (PPT > 0) {
     if constexpr (VAR == 1) return pcg_resident<PPT>(c, a, bnorm2, rz, its);
@@ -813,6 +931,188 @@ __device__ __forceinline__ int pcg_solve(GridCtx& c, const FusionArgs& a, const 
 }
 
 // ---------------------------------------------------------------------------
+// optimize() on the device (fusion.hpp:402-454). Ctx: GridCtx (one grid)
+// or BandCtx (row bands, hierarchical all-reduce); every CTA runs the same
+// control flow on identical all-reduced scalars.
+template <int PPT, int VAR, class Ctx>
+__device__ __forceinline__ void optimize_body(Ctx& c, const FusionArgs& a, const Range& rg,
+                                              const Sel& sel, const bool leader, int& status) {
+  constexpr int SU = PPT > 0 ? PPT : 2;  // pixels per thread per unrolled sweep group
+  FusionControl* ctl = a.ctl;
+  const FusionStateDev st0 = *a.st_in;
+  double scale = st0.scale;
+  int iteration = st0.iteration;
+  int cur = st0.cur;
+  const int inliers = a.inlier_dev ? *a.inlier_dev : a.inlier_count;
+  const bool ls_mode = a.mode == DFUSE_MODE_LSSCALE;
+  const bool depth_solvable = !ls_mode || inliers > 0;
+  int cost_evals = 0, pcg_total = 0, gn_done = 0;
+  const bool otr = a.trace && leader;  // DFUSE_TRACE: ns per GN phase, CTA 0
+  __shared__ long long ot[8];          // [7] = last timestamp (thread 0 only)
+  if (otr)
+    for (int k = 0; k < 8; ++k) ot[k] = 0;
+#define DF_OTRACE(k)                \
+if (otr) {                        \
+  const long long t_ = df_now(); \
+  ot[k] += t_ - ot[7];            \
+  ot[7] = t_;                     \
+}
+  for (int it = 0; it < a.gn && status == 0; ++it) {
+    if (otr) ot[7] = df_now();
+    bool have_eq = false;  // the scale block left an assembly valid for the depth block
+    double veq[4] = {0.0, 0.0, 0.0, 0.0};
+    if (!ls_mode && a.est_scale && inliers > 0) {  // fusion.hpp:411-425
+      const double ln_s0 = log(scale);
+      double ln_s = ln_s0;
+      double c0 = 0.0;
+      extern __shared__ double dsm_stage[];
+      double* stage = a.stage_n > 0 ? dsm_stage : nullptr;
+      // the scale sweeps write no global memory, so their all-reduces need
+      // no fence
+      for (int round = 0; round < 3; ++round) {
+        if (round == 0) {
+          double v[4];
+          sweep_scale<SU>(a, sel, rg, a.ld[cur], ln_s, true, sel.scale ? ln_s0 : 0.0, v, stage,
+                          a.stage_n);
+          double w[3] = {v[0], v[1], v[2]};
+          grid_allreduce<3, false>(c, w);
+          c0 = w[2];
+          ln_s = w[0] / w[1];
+        } else {
+          double w[2];
+          if (stage) {
+            sweep_scale_staged(a, rg, stage, a.stage_n, ln_s, w);
+          } else {
+            double v[4];
+            sweep_scale<SU>(a, sel, rg, a.ld[cur], ln_s, false, 0.0, v);
+            w[0] = v[0];
+            w[1] = v[1];
+          }
+          grid_allreduce<2, false>(c, w);
+          ln_s = w[0] / w[1];
+        }
+      }
+      cost_evals += 1;
+      DF_OTRACE(0);
+      const double s_new = exp(ln_s);
+      const double dlns = log(s_new) - log(scale);
+      double step = 1.0, accepted = 0.0;
+      for (int half = 0; half <= 5; ++half) {
+        const double ts = exp(log(scale) + step * dlns);
+        double tc;
+        if (half == 0 && depth_solvable) {
+          // The full step is accepted almost always, and the depth block
+          // then assembles at exactly this (state, scale) and starts from
+          // exactly this cost (fusion.hpp:426-429). So the first trial's
+          // sweep assembles the normal equations speculatively; its cost
+          // is the trial cost, and on acceptance the assembly stands.
+          double v[4];
+          sweep_assemble<SU>(a, sel, rg, a.ld[cur], sel.scale ? log(ts) : 0.0, false, v);
+          grid_allreduce(c, v);  // fenced: the PCG reads the assembled rasters
+          tc = v[3];
+          if (tc <= c0) {
+            have_eq = true;
+            for (int k = 0; k < 4; ++k) veq[k] = v[k];
+          }
+        } else {
+          double v[1] = {sweep_cost<SU>(a, sel, rg, PlainLd{a.ld[cur]},
+                                        sel.scale ? log(ts) : 0.0, nullptr)};
+          DF_OTRACE(5);
+          grid_allreduce<1, false>(c, v);
+          tc = v[0];
+        }
+        cost_evals += 1;
+        if (tc <= c0) {
+          scale = ts;
+          accepted = step;
+          break;
+        }
+        step *= 0.5;
+      }
+      if (leader && it < DFUSE_STATS_MAX_GN) ctl->stats.scale_step[it] = accepted;
+      DF_OTRACE(1);
+    }
+    if (depth_solvable) {  // fusion.hpp:426-441
+      const double ln_s = sel.scale ? log(scale) : 0.0;
+      double v[4];
+      if (have_eq) {  // assembled by the accepted scale trial
+        for (int k = 0; k < 4; ++k) v[k] = veq[k];
+      } else {
+        sweep_assemble<SU>(a, sel, rg, a.ld[cur], ln_s, false, v);
+        grid_allreduce(c, v);
+      }
+      const double c0 = v[3];
+      cost_evals += 1;
+      DF_OTRACE(2);
+      int its = 0;
+      if (v[0] != 0.0) {
+        if (v[2] > 0.0) {
+          status = DFUSE_E_CG_DIVERGENCE;
+        } else {
+          status = pcg_solve<PPT, VAR>(c, a, rg, v[0], v[1], &its);
+        }
+      }
+      DF_OTRACE(3);
+      pcg_total += its;
+      if (leader && it < DFUSE_STATS_MAX_GN) ctl->stats.pcg_iters[it] = its;
+      if (status) break;
+      double step = 1.0, accepted = 0.0;
+      const bool xzero = its == 0;  // delta == 0 (b == 0 or cg_max_iters == 0)
+      for (int half = 0; half <= 5; ++half) {
+        double w[1];
+        if (xzero)
+          w[0] = sweep_cost<SU>(a, sel, rg, PlainLd{a.ld[cur]}, ln_s, a.ld[1 - cur]);
+        else
+          w[0] = sweep_cost<SU>(a, sel, rg, TrialLd{a.ld[cur], a.x, step}, ln_s, a.ld[1 - cur]);
+        DF_OTRACE(6);
+        grid_allreduce(c, w);
+        cost_evals += 1;
+        if (w[0] <= c0) {
+          cur = 1 - cur;
+          accepted = step;
+          break;
+        }
+        step *= 0.5;
+      }
+      if (leader && it < DFUSE_STATS_MAX_GN) ctl->stats.depth_step[it] = accepted;
+      DF_OTRACE(4);
+    }
+    iteration += 1;
+    gn_done = it + 1;
+  }
+#undef DF_OTRACE
+  if (otr)
+    for (int k = 0; k < 7; ++k) ctl->trace[8 + k] = ot[k];
+  if (status == 0 && ls_mode) {  // fusion.hpp:445-452
+    double v[1] = {0.0};
+    const double* ld = a.ld[cur];
+    for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) v[0] += a.pred[0][i] - ld[i];
+    grid_allreduce(c, v);
+    const double offset = v[0] / (double)((long)a.W * a.H);
+    double* ldw = a.ld[cur];
+    for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) {
+      ldw[i] += offset;
+      halo_put(a, cur ? HP_LD1 : HP_LD0, i, ldw[i]);
+    }
+    scale = exp(offset);
+  }
+  if (leader) {
+    FusionStateDev out = st0;  // transactional: unchanged on error
+    if (status == 0) {
+      out.scale = scale;
+      out.iteration = iteration;
+      out.cur = cur;
+    }
+    *a.st_out = out;
+    ctl->scale = out.scale;
+    ctl->iteration = out.iteration;
+    ctl->ld_final = out.cur;
+    ctl->stats.gn_done = gn_done;
+    ctl->stats.pcg_total = pcg_total;
+    ctl->stats.cost_evals = cost_evals;
+  }
+}
+
 // PPT: pixels per thread of the SM-resident PCG (0 = streaming PCG);
 // VAR: resident PCG variant (0 pipelined, 1 Chronopoulos-Gear, 2 two
 // all-reduces). One instantiation per (PPT, VAR) keeps each kernel's code
@@ -883,180 +1183,78 @@ __global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
     }
     if (leader) ctl->pcg_last = its;
   } else {  // OP_OPTIMIZE, fusion.hpp:402-454
-    const FusionStateDev st0 = *a.st_in;
-    double scale = st0.scale;
-    int iteration = st0.iteration;
-    int cur = st0.cur;
-    const int inliers = a.inlier_dev ? *a.inlier_dev : a.inlier_count;
-    const bool ls_mode = a.mode == DFUSE_MODE_LSSCALE;
-    const bool depth_solvable = !ls_mode || inliers > 0;
-    int cost_evals = 0, pcg_total = 0, gn_done = 0;
-    const bool otr = a.trace && leader;  // DFUSE_TRACE: ns per GN phase, CTA 0
-    __shared__ long long ot[8];          // [7] = last timestamp (thread 0 only)
-    if (otr)
-      for (int k = 0; k < 8; ++k) ot[k] = 0;
-#define DF_OTRACE(k)                \
-  if (otr) {                        \
-    const long long t_ = df_now(); \
-    ot[k] += t_ - ot[7];            \
-    ot[7] = t_;                     \
-  }
-    for (int it = 0; it < a.gn && status == 0; ++it) {
-      if (otr) ot[7] = df_now();
-      bool have_eq = false;  // the scale block left an assembly valid for the depth block
-      double veq[4] = {0.0, 0.0, 0.0, 0.0};
-      if (!ls_mode && a.est_scale && inliers > 0) {  // fusion.hpp:411-425
-        const double ln_s0 = log(scale);
-        double ln_s = ln_s0;
-        double c0 = 0.0;
-        extern __shared__ double dsm_stage[];
-        double* stage = a.stage_n > 0 ? dsm_stage : nullptr;
-        // the scale sweeps write no global memory, so their all-reduces need
-        // no fence
-        for (int round = 0; round < 3; ++round) {
-          if (round == 0) {
-            double v[4];
-            sweep_scale<SU>(a, sel, rg, a.ld[cur], ln_s, true, sel.scale ? ln_s0 : 0.0, v, stage,
-                            a.stage_n);
-            double w[3] = {v[0], v[1], v[2]};
-            grid_allreduce<3, false>(c, w);
-            c0 = w[2];
-            ln_s = w[0] / w[1];
-          } else {
-            double w[2];
-            if (stage) {
-              sweep_scale_staged(a, rg, stage, a.stage_n, ln_s, w);
-            } else {
-              double v[4];
-              sweep_scale<SU>(a, sel, rg, a.ld[cur], ln_s, false, 0.0, v);
-              w[0] = v[0];
-              w[1] = v[1];
-            }
-            grid_allreduce<2, false>(c, w);
-            ln_s = w[0] / w[1];
-          }
-        }
-        cost_evals += 1;
-        DF_OTRACE(0);
-        const double s_new = exp(ln_s);
-        const double dlns = log(s_new) - log(scale);
-        double step = 1.0, accepted = 0.0;
-        for (int half = 0; half <= 5; ++half) {
-          const double ts = exp(log(scale) + step * dlns);
-          double tc;
-          if (half == 0 && depth_solvable) {
-            // The full step is accepted almost always, and the depth block
-            // then assembles at exactly this (state, scale) and starts from
-            // exactly this cost (fusion.hpp:426-429). So the first trial's
-            // sweep assembles the normal equations speculatively; its cost
-            // is the trial cost, and on acceptance the assembly stands.
-            double v[4];
-            sweep_assemble<SU>(a, sel, rg, a.ld[cur], sel.scale ? log(ts) : 0.0, false, v);
-            grid_allreduce(c, v);  // fenced: the PCG reads the assembled rasters
-            tc = v[3];
-            if (tc <= c0) {
-              have_eq = true;
-              for (int k = 0; k < 4; ++k) veq[k] = v[k];
-            }
-          } else {
-            double v[1] = {sweep_cost<SU>(a, sel, rg, PlainLd{a.ld[cur]},
-                                          sel.scale ? log(ts) : 0.0, nullptr)};
-            DF_OTRACE(5);
-            grid_allreduce<1, false>(c, v);
-            tc = v[0];
-          }
-          cost_evals += 1;
-          if (tc <= c0) {
-            scale = ts;
-            accepted = step;
-            break;
-          }
-          step *= 0.5;
-        }
-        if (leader && it < DFUSE_STATS_MAX_GN) ctl->stats.scale_step[it] = accepted;
-        DF_OTRACE(1);
-      }
-      if (depth_solvable) {  // fusion.hpp:426-441
-        const double ln_s = sel.scale ? log(scale) : 0.0;
-        double v[4];
-        if (have_eq) {  // assembled by the accepted scale trial
-          for (int k = 0; k < 4; ++k) v[k] = veq[k];
-        } else {
-          sweep_assemble<SU>(a, sel, rg, a.ld[cur], ln_s, false, v);
-          grid_allreduce(c, v);
-        }
-        const double c0 = v[3];
-        cost_evals += 1;
-        DF_OTRACE(2);
-        int its = 0;
-        if (v[0] != 0.0) {
-          if (v[2] > 0.0) {
-            status = DFUSE_E_CG_DIVERGENCE;
-          } else {
-            status = pcg_solve<PPT, VAR>(c, a, rg, v[0], v[1], &its);
-          }
-        }
-        DF_OTRACE(3);
-        pcg_total += its;
-        if (leader && it < DFUSE_STATS_MAX_GN) ctl->stats.pcg_iters[it] = its;
-        if (status) break;
-        double step = 1.0, accepted = 0.0;
-        const bool xzero = its == 0;  // delta == 0 (b == 0 or cg_max_iters == 0)
-        for (int half = 0; half <= 5; ++half) {
-          double w[1];
-          if (xzero)
-            w[0] = sweep_cost<SU>(a, sel, rg, PlainLd{a.ld[cur]}, ln_s, a.ld[1 - cur]);
-          else
-            w[0] = sweep_cost<SU>(a, sel, rg, TrialLd{a.ld[cur], a.x, step}, ln_s, a.ld[1 - cur]);
-          DF_OTRACE(6);
-          grid_allreduce(c, w);
-          cost_evals += 1;
-          if (w[0] <= c0) {
-            cur = 1 - cur;
-            accepted = step;
-            break;
-          }
-          step *= 0.5;
-        }
-        if (leader && it < DFUSE_STATS_MAX_GN) ctl->stats.depth_step[it] = accepted;
-        DF_OTRACE(4);
-      }
-      iteration += 1;
-      gn_done = it + 1;
-    }
-#undef DF_OTRACE
-    if (otr)
-      for (int k = 0; k < 7; ++k) ctl->trace[8 + k] = ot[k];
-    if (status == 0 && ls_mode) {  // fusion.hpp:445-452
-      double v[1] = {0.0};
-      const double* ld = a.ld[cur];
-      for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) v[0] += a.pred[0][i] - ld[i];
-      grid_allreduce(c, v);
-      const double offset = v[0] / (double)((long)a.W * a.H);
-      double* ldw = a.ld[cur];
-      for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) ldw[i] += offset;
-      scale = exp(offset);
-    }
-    if (leader) {
-      FusionStateDev out = st0;  // transactional: unchanged on error
-      if (status == 0) {
-        out.scale = scale;
-        out.iteration = iteration;
-        out.cur = cur;
-      }
-      *a.st_out = out;
-      ctl->scale = out.scale;
-      ctl->iteration = out.iteration;
-      ctl->ld_final = out.cur;
-      ctl->stats.gn_done = gn_done;
-      ctl->stats.pcg_total = pcg_total;
-      ctl->stats.cost_evals = cost_evals;
-    }
+    optimize_body<PPT, VAR>(c, a, rg, sel, leader, status);
   }
   if (leader) {
     ctl->status = status;
     ctl->stats.grid_syncs = c.syncs;
   }
+}
+
+// optimize() over row bands: CTAs [b cpr, (b+1) cpr)
+// of this launch run band band0 + b with that band's FusionArgs, the
+// streaming PCG and the two-level all-reduce of BandCtx. One launch holding
+// every band is the single-GPU form of the multi-GPU layout (the bands'
+// planes are separate allocations that exchange halo rows and band totals
+// only through the BandNb pointers and the level-2 LL arrays, which on
+// several GPUs are peer mappings).
+struct BandLaunch {
+  const FusionArgs* args;                  // [nband]
+  unsigned long long* const* rank_slots;   // [nband] level-2 LL arrays
+  int nband, cpr, band0, sys;
+};
+
+__global__ void __launch_bounds__(FT, 1) k_fusion_banded(BandLaunch L) {
+  __shared__ FusionArgs s_args;  // fields survive the L1 invalidation of every fence
+  const int band = L.band0 + (int)(blockIdx.x / L.cpr);
+  if (threadIdx.x == 0) s_args = L.args[band];
+  __syncthreads();
+  const FusionArgs& a = s_args;
+  BandCtx c;
+  c.slots = a.slots;
+  c.G = (unsigned)L.cpr;
+  c.base_tag = 0;
+  c.phase = 0;
+  c.syncs = 0;
+  c.ll_next = 1;
+  c.me = blockIdx.x % L.cpr;
+  c.band = band;
+  c.nband = L.nband;
+  c.rank_slots = L.rank_slots;
+  c.sys = L.sys;
+  const Range rg = my_range(a);
+  const Sel sel = terms_for(a.mode);
+  FusionControl* ctl = a.ctl;
+  const bool leader = c.me == 0 && threadIdx.x == 0;  // each band's own control block
+  if (c.me == 0) {
+    for (int k = threadIdx.x; k < DFUSE_STATS_MAX_GN; k += FT) {
+      ctl->stats.pcg_iters[k] = -1;
+      ctl->stats.scale_step[k] = -1.0;
+      ctl->stats.depth_step[k] = -1.0;
+    }
+    __syncthreads();
+  }
+  sweep_prologue(a, rg);
+  grid_sync(c);  // fenced: the per-call planes (and their halo rows) are read at i-1, i-W
+  int status = 0;
+  optimize_body<0, 0>(c, a, rg, sel, leader, status);
+  if (leader) {
+    ctl->status = status;
+    ctl->stats.grid_syncs = c.syncs;
+  }
+}
+
+void launch_fusion_banded(dfuse_ctx* ctx, const FusionArgs* args_dev,
+                          unsigned long long* const* rank_slots_dev, int nband, int cpr) {
+  BandLaunch L{args_dev, rank_slots_dev, nband, cpr, 0, 0};
+  void* argv[] = {&L};
+  DF_CUDA(cudaLaunchCooperativeKernel((const void*)k_fusion_banded, dim3(nband * cpr), dim3(FT),
+                                      argv, 0, ctx->stream));
+  DF_LAUNCHED(ctx);
+}
+
+size_t band_rank_slots_bytes(int nband) {
+  return sizeof(unsigned long long) * kSlotWords * 8 * (size_t)nband;
 }
 
 // cost_gradient in gather form (fusion.hpp:274-305). The gradient at pixel

@@ -33,6 +33,20 @@ struct FusionControl {
   dfuse_solver_stats stats;
 };
 
+// Row-band decomposition of one keyframe: band g
+// owns rows [y0, y1). Each band's planes are separate allocations covering
+// rows [y0 - 1, y1 + 1) whose base pointers are shifted so that global pixel
+// indices address them; the planes read at i - W / i + W get their halo row
+// from the neighbour band, which writes its boundary row into both its own
+// plane and ours (a remote store when bands live on different GPUs).
+enum HaloPlane {
+  HP_LD0, HP_LD1, HP_X, HP_R, HP_DIAG, HP_DOWN, HP_P0, HP_P1, HP_IV2, HP_COUNT
+};
+struct BandNb {
+  double* up[HP_COUNT];  // the band above's plane (whose bottom halo row is our row y0), or null
+  double* dn[HP_COUNT];  // the band below's plane (whose top halo row is our row y1 - 1), or null
+};
+
 struct FusionArgs {
   int W, H;
   const double* pred[6];
@@ -70,6 +84,9 @@ struct FusionArgs {
   int stage_n;  // > 0: scale rounds 1-2 read round 0's values from shared memory
   long long* dbg;  // DFUSE_TRACE=2: per-CTA phase times [grid][8]
   FusionControl* ctl;
+  // row band (banded launches; otherwise y0 = 0, y1 = H, ctas = 0 = the grid)
+  int band_y0, band_y1, band_cta0, band_ctas;
+  const BandNb* nb;  // null unless banded
 };
 
 int fusion_grid(dfuse_ctx* ctx);
@@ -79,6 +96,11 @@ bool fusion_resident_possible(long P, int grid);
 float sync_bench(dfuse_ctx* ctx, int n, int variant, int grid);
 void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid);
 void launch_gradient(dfuse_ctx* ctx, FusionArgs& a, int grid, double* g);
+// row-band optimize: args_dev[nband] (device), one cooperative launch of
+// nband * cpr CTAs (fusion.cu, k_fusion_banded)
+void launch_fusion_banded(dfuse_ctx* ctx, const FusionArgs* args_dev,
+                          unsigned long long* const* rank_slots_dev, int nband, int cpr);
+size_t band_rank_slots_bytes(int nband);
 void launch_stencil_apply(dfuse_ctx* ctx, int W, int H, const double* diag, const double* right,
                           const double* down, const double* x, double* y);
 

@@ -42,7 +42,9 @@ void launch_photometric(dfuse_ctx* ctx, const dfuse_epigeom& g, const float* I0,
                         double x, double y, double d, double* out);
 void launch_texture_mask(dfuse_ctx* ctx, const float* img, int w, int h, double threshold,
                          uint8_t* mask);
-void launch_mask_list(dfuse_ctx* ctx, const uint8_t* mask, long P, int* list, int* count);
+// list = indices i (+ index_offset) of the set mask[i], i < P, in any order
+void launch_mask_list(dfuse_ctx* ctx, const uint8_t* mask, long P, int* list, int* count,
+                      long index_offset = 0);
 void launch_stereo(dfuse_ctx* ctx, const StereoArgs& a, bool list_mode);
 void launch_count_valid(dfuse_ctx* ctx, const uint8_t* valid, long P, int* out);
 void launch_compact_obs(dfuse_ctx* ctx, const uint8_t* flag, const dfuse_obs* dense, long P,
