@@ -305,6 +305,27 @@ int dfuse_bkf_download(dfuse_banded_keyframe* kf, double* log_depth, double* sca
                        int32_t* iteration, double* semi_depth, double* semi_variance,
                        uint8_t* semi_valid, int32_t* inlier_count, uint8_t* mask);
 
+/* Multi-GPU form (one process per GPU, `world` bands, this process computes
+ * band `rank`): create the band, exchange dfuse_band_peer records between the
+ * ranks (any transport: torch.distributed all_gather_object in
+ * paper_2207_12244_b200/bands_dist.py), connect. The neighbours' halo rows
+ * and the level-2 all-reduce arrays are then CUDA-IPC mappings of the peers'
+ * band allocations over NVLink, written with system-scope fences; every rank
+ * calls process_frame for the same frame and the ranks' kernels meet through
+ * those mappings. download returns this rank's rows (and its share of the
+ * observation / inlier counts); world == 1 needs no connect. */
+typedef struct {
+  char handle[64];  /* cudaIpcMemHandle_t of the band allocation */
+  int32_t cpr;      /* CTAs per band on that rank (sizes its all-reduce slots) */
+  int32_t y0, y1;   /* rows of the band */
+  int32_t width;
+} dfuse_band_peer;
+int dfuse_bkf_create_rank(dfuse_ctx* ctx, const dfuse_intrinsics* K, const float* I0,
+                          const double* const pred[6], double texture_threshold, int world,
+                          int rank, dfuse_banded_keyframe** out);
+int dfuse_bkf_peer_info(dfuse_banded_keyframe* kf, dfuse_band_peer* out);
+int dfuse_bkf_connect(dfuse_banded_keyframe* kf, const dfuse_band_peer* peers);
+
 /* ---- scoring (eval.hpp:34-68, 221-226; pipeline.hpp:232-247) --------- */
 typedef struct {
   double pct_within_10;   /* KeyframeScore::pct_correct */

@@ -29,12 +29,21 @@ namespace {
 
 size_t al(size_t v) { return (v + 255) & ~size_t(255); }
 
+enum BandPlane {  // the 24 double planes of a band, in allocation order
+  BP_PRED0 = 0, BP_SD = 6, BP_SV, BP_LNSD, BP_IRS, BP_IV0, BP_IV1, BP_IV2, BP_LD0, BP_LD1,
+  BP_DIAG, BP_RIGHT, BP_DOWN, BP_B, BP_X, BP_R, BP_P0, BP_P1, BP_Q, BP_COUNT
+};
+static_assert(BP_COUNT == 24, "plane count");
+
 struct Band {
   int y0 = 0, y1 = 0;
   void* block = nullptr;
+  bool owned = false;   // allocated here (else an IPC mapping of a peer's band, or absent)
+  bool local = false;   // computed by this process
   int* list = nullptr;
-  int* counters = nullptr;  // [0] work counter, [1] list length
+  int* counters = nullptr;  // [0] work counter, [1] list length, [2] n_obs, [3] inlier count
   int n_mask = 0;
+  int h_counters[2] = {0, 0};
   double *semi_d = nullptr, *semi_v = nullptr;
   uint8_t* semi_valid = nullptr;
   unsigned long long* rank_slots = nullptr;
@@ -49,19 +58,20 @@ struct Band {
 struct dfuse_banded_keyframe {
   dfuse_ctx* ctx = nullptr;
   int W = 0, H = 0, nband = 0, cpr = 0;
+  int rank = -1;      // -1: every band in this process; else the one band it computes
+  bool connected = false;  // neighbours and level-2 arrays bound (dfuse_bkf_connect)
   long P = 0;
   void* common = nullptr;  // I0, I1, mask, shared counters, device arg arrays
   float* I0 = nullptr;
   float* I1 = nullptr;
   uint8_t* mask = nullptr;
-  int* shared = nullptr;  // [0] n_obs, [1] inlier_count
+  int* shared = nullptr;  // unused (per-band counters)
   FusionArgs* d_args = nullptr;
   unsigned long long** d_rank = nullptr;
   std::vector<Band> bands;
   int parity = 0;
   int stereo_frames = 0;
   FusionControl* h_ctl = nullptr;  // pinned
-  int* h_shared = nullptr;         // pinned
 };
 
 namespace {
@@ -88,38 +98,51 @@ int bkf_guarded(dfuse_banded_keyframe* kf, F&& f) {
 inline int lo_row(const Band& b) { return b.y0 > 0 ? b.y0 - 1 : 0; }
 inline int hi_row(const Band& b, int H) { return b.y1 < H ? b.y1 + 1 : H; }
 
-enum BandPlane {  // the 24 double planes of a band, in allocation order
-  BP_PRED0 = 0, BP_SD = 6, BP_SV, BP_LNSD, BP_IRS, BP_IV0, BP_IV1, BP_IV2, BP_LD0, BP_LD1,
-  BP_DIAG, BP_RIGHT, BP_DOWN, BP_B, BP_X, BP_R, BP_P0, BP_P1, BP_Q, BP_COUNT
-};
-static_assert(BP_COUNT == 24, "plane count");
 
-void alloc_band(dfuse_banded_keyframe* kf, Band& b) {
-  const int W = kf->W;
-  const long rows = b.y1 - b.y0 + 2;  // halo row on both sides (unused outside the image)
-  const long n = rows * W;
-  const size_t dP = al(sizeof(double) * n);
-  const size_t total = BP_COUNT * dP + al(n) + al(sizeof(int) * (size_t)(b.y1 - b.y0) * W) + 256 +
-                       al(fusion_slots_bytes(kf->cpr)) + al(band_rank_slots_bytes(kf->nband)) +
-                       al(sizeof(FusionControl)) + al(2 * sizeof(FusionStateDev)) +
-                       al(sizeof(BandNb));
-  DF_CUDA(cudaMalloc(&b.block, total));
-  char* p = (char*)b.block;
+
+// Byte layout of one band's allocation: a pure function of (W, rows, CTAs
+// per band, band count), so a peer can rebuild every pointer of a band it
+// maps by IPC from the base address alone.
+struct BandLayout {
+  size_t plane[BP_COUNT], valid, list, counters, slots, rank_slots, ctl, st, nb, total;
+};
+
+BandLayout band_layout(int W, int y0, int y1, int cpr, int nband) {
+  BandLayout L;
+  const long n = (long)(y1 - y0 + 2) * W;  // halo row on both sides
+  size_t o = 0;
   auto take = [&](size_t bytes) {
-    char* r = p;
-    p += al(bytes);
-    return (void*)r;
+    const size_t r = o;
+    o += al(bytes);
+    return r;
   };
+  for (int k = 0; k < BP_COUNT; ++k) L.plane[k] = take(sizeof(double) * n);
+  L.valid = take(n);
+  L.list = take(sizeof(int) * (size_t)(y1 - y0) * W);
+  L.counters = take(256);
+  L.slots = take(fusion_slots_bytes(cpr));
+  L.rank_slots = take(band_rank_slots_bytes(nband));
+  L.ctl = take(sizeof(FusionControl));
+  L.st = take(2 * sizeof(FusionStateDev));
+  L.nb = take(sizeof(BandNb));
+  L.total = o;
+  return L;
+}
+
+// point b (and b.fa) into the band allocation at `base`
+void bind_band(dfuse_banded_keyframe* kf, Band& b, char* base, int cpr) {
+  const int W = kf->W;
+  const BandLayout L = band_layout(W, b.y0, b.y1, cpr, kf->nband);
+  b.block = base;
   const long shift = (long)(b.y0 - 1) * W;  // plane + shift addresses row y0 - 1 at index 0
   double* sh[BP_COUNT];
   for (int k = 0; k < BP_COUNT; ++k) {
-    b.plane_base[k] = (double*)take(sizeof(double) * n);
+    b.plane_base[k] = (double*)(base + L.plane[k]);
     sh[k] = b.plane_base[k] - shift;
   }
-  uint8_t* valid = (uint8_t*)take(n);
-  b.semi_valid = valid - shift;
-  b.list = (int*)take(sizeof(int) * (size_t)(b.y1 - b.y0) * W);
-  b.counters = (int*)take(256);
+  b.semi_valid = (uint8_t*)(base + L.valid) - shift;
+  b.list = (int*)(base + L.list);
+  b.counters = (int*)(base + L.counters);
   FusionArgs& f = b.fa;
   memset(&f, 0, sizeof f);
   f.W = kf->W;
@@ -144,16 +167,24 @@ void alloc_band(dfuse_banded_keyframe* kf, Band& b) {
   f.p[0] = sh[BP_P0];
   f.p[1] = sh[BP_P1];
   f.q = sh[BP_Q];
-  f.slots = (ReduceSlot*)take(fusion_slots_bytes(kf->cpr));
-  b.rank_slots = (unsigned long long*)take(band_rank_slots_bytes(kf->nband));
-  f.ctl = (FusionControl*)take(sizeof(FusionControl));
-  b.st = (FusionStateDev*)take(2 * sizeof(FusionStateDev));
-  b.nb_dev = (BandNb*)take(sizeof(BandNb));
-  f.inlier_dev = kf->shared + 1;
+  f.slots = (ReduceSlot*)(base + L.slots);
+  b.rank_slots = (unsigned long long*)(base + L.rank_slots);
+  f.ctl = (FusionControl*)(base + L.ctl);
+  b.st = (FusionStateDev*)(base + L.st);
+  b.nb_dev = (BandNb*)(base + L.nb);
+  f.inlier_dev = b.counters + 3;  // the band's own inlier count (summed in the kernel)
   f.band_y0 = b.y0;
   f.band_y1 = b.y1;
-  f.band_ctas = kf->cpr;
+  f.band_ctas = cpr;
   f.nb = b.nb_dev;
+}
+
+void alloc_band(dfuse_banded_keyframe* kf, Band& b) {
+  const BandLayout L = band_layout(kf->W, b.y0, b.y1, kf->cpr, kf->nband);
+  void* base = nullptr;
+  DF_CUDA(cudaMalloc(&base, L.total));
+  b.owned = true;
+  bind_band(kf, b, (char*)base, kf->cpr);
   DF_CUDA(cudaMemsetAsync(b.counters, 0, 256, kf->ctx->stream));
 }
 
@@ -181,6 +212,7 @@ void reset_bkf(dfuse_banded_keyframe* kf) {
   dfuse_ctx* ctx = kf->ctx;
   const int W = kf->W;
   for (Band& b : kf->bands) {
+    if (!b.local) continue;
     const long n = (long)(b.y1 - b.y0 + 2) * W;
     DF_CUDA(cudaMemsetAsync(b.plane_base[BP_SD], 0, sizeof(double) * n, ctx->stream));
     DF_CUDA(cudaMemsetAsync(b.plane_base[BP_SV], 0, sizeof(double) * n, ctx->stream));
@@ -191,8 +223,8 @@ void reset_bkf(dfuse_banded_keyframe* kf) {
                             cudaMemcpyDeviceToDevice, ctx->stream));
     FusionStateDev s0{1.0, 0, 0};
     DF_CUDA(cudaMemcpyAsync(b.st, &s0, sizeof s0, cudaMemcpyHostToDevice, ctx->stream));
+    DF_CUDA(cudaMemsetAsync(b.counters + 2, 0, 2 * sizeof(int), ctx->stream));
   }
-  DF_CUDA(cudaMemsetAsync(kf->shared, 0, 2 * sizeof(int), ctx->stream));
   DF_CUDA(cudaStreamSynchronize(ctx->stream));
   kf->parity = 0;
   kf->stereo_frames = 0;
@@ -214,8 +246,10 @@ void process_bkf(dfuse_banded_keyframe* kf, const dfuse_epigeom* g, const float*
   }
   // stereo stage: every band scans its own masked pixels (pipeline.hpp:205-213)
   DF_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
-  DF_CUDA(cudaMemsetAsync(kf->shared, 0, sizeof(int), ctx->stream));  // n_obs
+  if (!kf->connected) throw RefError{DFUSE_E_INVALID_ARGUMENT, "bands not connected"};
   for (Band& b : kf->bands) {
+    if (!b.local) continue;
+    DF_CUDA(cudaMemsetAsync(b.counters + 2, 0, sizeof(int), ctx->stream));  // n_obs
     if (b.n_mask == 0) continue;
     StereoArgs a;
     memset(&a, 0, sizeof a);
@@ -229,15 +263,18 @@ void process_bkf(dfuse_banded_keyframe* kf, const dfuse_epigeom* g, const float*
     a.depth = b.semi_d;
     a.variance = b.semi_v;
     a.valid = b.semi_valid;
-    a.n_obs = kf->shared;
-    a.n_installed = kf->shared + 1;
+    a.n_obs = b.counters + 2;
+    a.n_installed = b.counters + 3;
     launch_stereo(ctx, a, false);
   }
   DF_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
   // optimise stage over all bands (pipeline.hpp:223-226)
   std::vector<FusionArgs> args(kf->nband);
+  int first = -1, nlocal = 0;
   for (int k = 0; k < kf->nband; ++k) {
     Band& b = kf->bands[k];
+    if (!b.local) continue;
+    if (first < 0) first = k;
     FusionArgs f = b.fa;
     f.dsemi = rcfg->delta_semi;
     f.dnet = rcfg->delta_net;
@@ -250,31 +287,133 @@ void process_bkf(dfuse_banded_keyframe* kf, const dfuse_epigeom* g, const float*
     f.op = OP_OPTIMIZE;
     f.st_in = b.st + kf->parity;
     f.st_out = b.st + (1 - kf->parity);
-    f.band_cta0 = k * kf->cpr;
+    f.band_cta0 = (k - first) * kf->cpr;
     args[k] = f;
-    // LL flags restart at 1 every launch
+    ++nlocal;
+    // LL flags restart at 1 every launch (every rank clears its own arrays
+    // before the launch; peers post into them only from inside theirs)
     DF_CUDA(cudaMemsetAsync(f.slots, 0, fusion_slots_bytes(kf->cpr), ctx->stream));
     DF_CUDA(cudaMemsetAsync(b.rank_slots, 0, band_rank_slots_bytes(kf->nband), ctx->stream));
   }
   DF_CUDA(cudaMemcpyAsync(kf->d_args, args.data(), sizeof(FusionArgs) * kf->nband,
                           cudaMemcpyHostToDevice, ctx->stream));
-  launch_fusion_banded(ctx, kf->d_args, kf->d_rank, kf->nband, kf->cpr);
+  launch_fusion_banded(ctx, kf->d_args, kf->d_rank, kf->nband, kf->cpr, first, nlocal,
+                       kf->rank >= 0 ? 1 : 0);
   DF_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
-  DF_CUDA(cudaMemcpyAsync(kf->h_shared, kf->shared, 2 * sizeof(int), cudaMemcpyDeviceToHost,
-                          ctx->stream));
-  DF_CUDA(cudaMemcpyAsync(kf->h_ctl, kf->bands[0].fa.ctl, sizeof(FusionControl),
+  for (Band& b : kf->bands)
+    if (b.local)
+      DF_CUDA(cudaMemcpyAsync(b.h_counters, b.counters + 2, 2 * sizeof(int),
+                              cudaMemcpyDeviceToHost, ctx->stream));
+  DF_CUDA(cudaMemcpyAsync(kf->h_ctl, kf->bands[first].fa.ctl, sizeof(FusionControl),
                           cudaMemcpyDeviceToHost, ctx->stream));
   DF_CUDA(cudaStreamSynchronize(ctx->stream));
+  int n_obs = 0, inliers = 0;
+  for (Band& b : kf->bands)
+    if (b.local) {
+      n_obs += b.h_counters[0];
+      inliers += b.h_counters[1];
+    }
   kf->parity = 1 - kf->parity;
-  const int n_obs = kf->h_shared[0];
+  // multi-process: these are this rank's bands (the caller sums over ranks)
   if (n_obs > 0) kf->stereo_frames += 1;  // pipeline.hpp:211
   res->observations = n_obs;
-  res->inlier_count = kf->h_shared[1];
+  res->inlier_count = inliers;
   res->stereo_frames = kf->stereo_frames;
   res->optimize_status = kf->h_ctl->status;
   DF_CUDA(cudaEventElapsedTime(&res->stereo_ms, ctx->ev[0], ctx->ev[1]));
   DF_CUDA(cudaEventElapsedTime(&res->optimise_ms, ctx->ev[1], ctx->ev[2]));
   res->stats = kf->h_ctl->stats;
+}
+
+}  // namespace
+
+namespace {
+
+void bind_neighbours(dfuse_banded_keyframe* kf) {
+  dfuse_ctx* ctx = kf->ctx;
+  std::vector<unsigned long long*> rank(kf->nband);
+  for (int g = 0; g < kf->nband; ++g) rank[g] = kf->bands[g].rank_slots;
+  for (int g = 0; g < kf->nband; ++g) {
+    Band& b = kf->bands[g];
+    if (!b.local) continue;
+    const BandNb nb = neighbours(kf, g);
+    DF_CUDA(cudaMemcpyAsync(b.nb_dev, &nb, sizeof nb, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  DF_CUDA(cudaMemcpyAsync(kf->d_rank, rank.data(), sizeof(void*) * kf->nband,
+                          cudaMemcpyHostToDevice, ctx->stream));
+  DF_CUDA(cudaStreamSynchronize(ctx->stream));
+  kf->connected = true;
+}
+
+// everything up to (not including) the neighbour binding; bands with
+// local = true are allocated and initialised here
+void create_bkf(dfuse_banded_keyframe* kf, const dfuse_intrinsics* K, const float* I0,
+                const double* const pred[6], double texture_threshold, int bands, int rank) {
+  dfuse_ctx* ctx = kf->ctx;
+  if (!K || !I0 || !pred) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null pointer"};
+  for (int c = 0; c < 6; ++c)
+    if (!pred[c]) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null prediction plane"};
+  if (K->width <= 0 || K->height <= 0)
+    throw RefError{DFUSE_E_INVALID_ARGUMENT, "raster dimensions must be positive"};
+  if (texture_threshold <= 0.0)
+    throw RefError{DFUSE_E_INVALID_ARGUMENT, "texture threshold must be > 0"};
+  const int per_process = rank < 0 ? bands : 1;
+  if (bands < 1 || bands > K->height || per_process > ctx->num_sms ||
+      (rank >= 0 && rank >= bands))
+    throw RefError{DFUSE_E_INVALID_ARGUMENT, "bands must be in [1, min(height, SMs)]"};
+  kf->W = K->width;
+  kf->H = K->height;
+  kf->P = (long)kf->W * kf->H;
+  kf->nband = bands;
+  kf->rank = rank;
+  kf->cpr = fusion_grid(ctx) / per_process;  // CTAs per band (one per SM overall)
+  const long P = kf->P;
+  const size_t common = 2 * al(sizeof(float) * P) + al(P) + 256 +
+                        al(sizeof(FusionArgs) * bands) + al(sizeof(void*) * bands);
+  DF_CUDA(cudaMalloc(&kf->common, common));
+  char* p = (char*)kf->common;
+  auto take = [&](size_t bytes) {
+    char* r = p;
+    p += al(bytes);
+    return (void*)r;
+  };
+  kf->I0 = (float*)take(sizeof(float) * P);
+  kf->I1 = (float*)take(sizeof(float) * P);
+  kf->mask = (uint8_t*)take(P);
+  kf->shared = (int*)take(256);
+  kf->d_args = (FusionArgs*)take(sizeof(FusionArgs) * bands);
+  kf->d_rank = (unsigned long long**)take(sizeof(void*) * bands);
+  DF_CUDA(cudaMallocHost(&kf->h_ctl, sizeof(FusionControl)));
+  kf->bands.resize(bands);
+  for (int g = 0; g < bands; ++g) {  // even row split
+    Band& b = kf->bands[g];
+    b.y0 = (int)((long)kf->H * g / bands);
+    b.y1 = (int)((long)kf->H * (g + 1) / bands);
+    b.local = rank < 0 || rank == g;
+    if (b.local) alloc_band(kf, b);
+  }
+  for (Band& b : kf->bands) {
+    if (!b.local) continue;
+    // predictions: the band's rows and its halo rows (pred[4] is read at i - W)
+    const int r0 = lo_row(b), r1 = hi_row(b, kf->H);
+    for (int c = 0; c < 6; ++c)
+      DF_CUDA(cudaMemcpyAsync((double*)b.fa.pred[c] + (long)r0 * kf->W,
+                              pred[c] + (long)r0 * kf->W,
+                              sizeof(double) * (size_t)(r1 - r0) * kf->W, cudaMemcpyHostToDevice,
+                              ctx->stream));
+  }
+  DF_CUDA(cudaMemcpyAsync(kf->I0, I0, sizeof(float) * P, cudaMemcpyHostToDevice, ctx->stream));
+  // make_keyframe: texture_mask (pipeline.hpp:148), then each band's list
+  launch_texture_mask(ctx, kf->I0, kf->W, kf->H, texture_threshold, kf->mask);
+  for (Band& b : kf->bands) {
+    if (!b.local) continue;
+    const long off = (long)b.y0 * kf->W;
+    launch_mask_list(ctx, kf->mask + off, (long)(b.y1 - b.y0) * kf->W, b.list, b.counters + 1,
+                     off);
+    DF_CUDA(cudaMemcpyAsync(&b.n_mask, b.counters + 1, sizeof(int), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+  }
+  reset_bkf(kf);  // synchronises
 }
 
 }  // namespace
@@ -287,11 +426,12 @@ int dfuse_bkf_destroy(dfuse_banded_keyframe* kf) {
     cudaSetDevice(kf->ctx->device);
     cudaStreamSynchronize(kf->ctx->stream);
   }
-  for (Band& b : kf->bands)
-    if (b.block) cudaFree(b.block);
+  for (Band& b : kf->bands) {
+    if (b.owned && b.block) cudaFree(b.block);
+    else if (b.block) cudaIpcCloseMemHandle(b.block);
+  }
   if (kf->common) cudaFree(kf->common);
   if (kf->h_ctl) cudaFreeHost(kf->h_ctl);
-  if (kf->h_shared) cudaFreeHost(kf->h_shared);
   delete kf;
   return DFUSE_OK;
 }
@@ -305,71 +445,8 @@ int dfuse_bkf_create(dfuse_ctx* ctx, const dfuse_intrinsics* K, const float* I0,
   if (!kf) return DFUSE_E_CUDA;
   kf->ctx = ctx;
   const int rc = bkf_guarded(kf, [&] {
-    if (!K || !I0 || !pred) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null pointer"};
-    for (int c = 0; c < 6; ++c)
-      if (!pred[c]) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null prediction plane"};
-    if (K->width <= 0 || K->height <= 0)
-      throw RefError{DFUSE_E_INVALID_ARGUMENT, "raster dimensions must be positive"};
-    if (texture_threshold <= 0.0)
-      throw RefError{DFUSE_E_INVALID_ARGUMENT, "texture threshold must be > 0"};
-    if (bands < 1 || bands > K->height || bands > ctx->num_sms)
-      throw RefError{DFUSE_E_INVALID_ARGUMENT, "bands must be in [1, min(height, SMs)]"};
-    kf->W = K->width;
-    kf->H = K->height;
-    kf->P = (long)kf->W * kf->H;
-    kf->nband = bands;
-    kf->cpr = fusion_grid(ctx) / bands;  // CTAs per band (one per SM overall)
-    const long P = kf->P;
-    const size_t common = 2 * al(sizeof(float) * P) + al(P) + 256 +
-                          al(sizeof(FusionArgs) * bands) + al(sizeof(void*) * bands);
-    DF_CUDA(cudaMalloc(&kf->common, common));
-    char* p = (char*)kf->common;
-    auto take = [&](size_t bytes) {
-      char* r = p;
-      p += al(bytes);
-      return (void*)r;
-    };
-    kf->I0 = (float*)take(sizeof(float) * P);
-    kf->I1 = (float*)take(sizeof(float) * P);
-    kf->mask = (uint8_t*)take(P);
-    kf->shared = (int*)take(256);
-    kf->d_args = (FusionArgs*)take(sizeof(FusionArgs) * bands);
-    kf->d_rank = (unsigned long long**)take(sizeof(void*) * bands);
-    DF_CUDA(cudaMallocHost(&kf->h_ctl, sizeof(FusionControl)));
-    DF_CUDA(cudaMallocHost(&kf->h_shared, 8 * sizeof(int)));
-    kf->bands.resize(bands);
-    for (int g = 0; g < bands; ++g) {  // even row split
-      kf->bands[g].y0 = (int)((long)kf->H * g / bands);
-      kf->bands[g].y1 = (int)((long)kf->H * (g + 1) / bands);
-      alloc_band(kf, kf->bands[g]);
-    }
-    std::vector<unsigned long long*> rank(bands);
-    for (int g = 0; g < bands; ++g) {
-      Band& b = kf->bands[g];
-      rank[g] = b.rank_slots;
-      const BandNb nb = neighbours(kf, g);
-      DF_CUDA(cudaMemcpyAsync(b.nb_dev, &nb, sizeof nb, cudaMemcpyHostToDevice, ctx->stream));
-      // predictions: the band's rows and its halo rows (pred[4] is read at i - W)
-      const int r0 = lo_row(b), r1 = hi_row(b, kf->H);
-      for (int c = 0; c < 6; ++c)
-        DF_CUDA(cudaMemcpyAsync((double*)b.fa.pred[c] + (long)r0 * kf->W,
-                                pred[c] + (long)r0 * kf->W,
-                                sizeof(double) * (size_t)(r1 - r0) * kf->W,
-                                cudaMemcpyHostToDevice, ctx->stream));
-    }
-    DF_CUDA(cudaMemcpyAsync(kf->d_rank, rank.data(), sizeof(void*) * bands,
-                            cudaMemcpyHostToDevice, ctx->stream));
-    DF_CUDA(cudaMemcpyAsync(kf->I0, I0, sizeof(float) * P, cudaMemcpyHostToDevice, ctx->stream));
-    // make_keyframe: texture_mask (pipeline.hpp:148), then each band's list
-    launch_texture_mask(ctx, kf->I0, kf->W, kf->H, texture_threshold, kf->mask);
-    for (Band& b : kf->bands) {
-      const long off = (long)b.y0 * kf->W;
-      launch_mask_list(ctx, kf->mask + off, (long)(b.y1 - b.y0) * kf->W, b.list, b.counters + 1,
-                       off);
-      DF_CUDA(cudaMemcpyAsync(&b.n_mask, b.counters + 1, sizeof(int), cudaMemcpyDeviceToHost,
-                              ctx->stream));
-    }
-    reset_bkf(kf);  // synchronises
+    create_bkf(kf, K, I0, pred, texture_threshold, bands, -1);
+    bind_neighbours(kf);
   });
   if (rc) {
     dfuse_bkf_destroy(kf);
@@ -377,6 +454,62 @@ int dfuse_bkf_create(dfuse_ctx* ctx, const dfuse_intrinsics* K, const float* I0,
   }
   *out = kf;
   return DFUSE_OK;
+}
+
+int dfuse_bkf_create_rank(dfuse_ctx* ctx, const dfuse_intrinsics* K, const float* I0,
+                          const double* const pred[6], double texture_threshold, int world,
+                          int rank, dfuse_banded_keyframe** out) {
+  if (!ctx || !out) return DFUSE_E_INVALID_ARGUMENT;
+  *out = nullptr;
+  dfuse_banded_keyframe* kf = new (std::nothrow) dfuse_banded_keyframe();
+  if (!kf) return DFUSE_E_CUDA;
+  kf->ctx = ctx;
+  const int rc = bkf_guarded(kf, [&] {
+    if (rank < 0) throw RefError{DFUSE_E_INVALID_ARGUMENT, "rank must be >= 0"};
+    create_bkf(kf, K, I0, pred, texture_threshold, world, rank);
+    if (world == 1) bind_neighbours(kf);
+  });
+  if (rc) {
+    dfuse_bkf_destroy(kf);
+    return rc;
+  }
+  *out = kf;
+  return DFUSE_OK;
+}
+
+int dfuse_bkf_peer_info(dfuse_banded_keyframe* kf, dfuse_band_peer* out) {
+  return bkf_guarded(kf, [&] {
+    if (!out || kf->rank < 0) throw RefError{DFUSE_E_INVALID_ARGUMENT, "not a rank keyframe"};
+    const Band& b = kf->bands[kf->rank];
+    memset(out, 0, sizeof *out);
+    cudaIpcMemHandle_t h;
+    DF_CUDA(cudaIpcGetMemHandle(&h, b.block));
+    static_assert(sizeof h == sizeof out->handle, "IPC handle size");
+    memcpy(out->handle, &h, sizeof h);
+    out->cpr = kf->cpr;
+    out->y0 = b.y0;
+    out->y1 = b.y1;
+    out->width = kf->W;
+  });
+}
+
+int dfuse_bkf_connect(dfuse_banded_keyframe* kf, const dfuse_band_peer* peers) {
+  return bkf_guarded(kf, [&] {
+    if (!peers || kf->rank < 0) throw RefError{DFUSE_E_INVALID_ARGUMENT, "not a rank keyframe"};
+    for (int g = 0; g < kf->nband; ++g) {
+      Band& b = kf->bands[g];
+      const dfuse_band_peer& pi = peers[g];
+      if (pi.y0 != b.y0 || pi.y1 != b.y1 || pi.width != kf->W)
+        throw RefError{DFUSE_E_DIMENSION_MISMATCH, "peer band layout differs"};
+      if (b.local) continue;
+      cudaIpcMemHandle_t h;
+      memcpy(&h, pi.handle, sizeof h);
+      void* base = nullptr;
+      DF_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+      bind_band(kf, b, (char*)base, pi.cpr);
+    }
+    bind_neighbours(kf);
+  });
 }
 
 int dfuse_bkf_reset(dfuse_banded_keyframe* kf) {
@@ -409,12 +542,16 @@ int dfuse_bkf_download(dfuse_banded_keyframe* kf, double* log_depth, double* sca
                        uint8_t* semi_valid, int32_t* inlier_count, uint8_t* mask) {
   return bkf_guarded(kf, [&] {
     dfuse_ctx* ctx = kf->ctx;
+    int first = 0;
+    while (!kf->bands[first].local) ++first;
     FusionStateDev st;
-    DF_CUDA(cudaMemcpyAsync(&st, kf->bands[0].st + kf->parity, sizeof st,
+    DF_CUDA(cudaMemcpyAsync(&st, kf->bands[first].st + kf->parity, sizeof st,
                             cudaMemcpyDeviceToHost, ctx->stream));
     DF_CUDA(cudaStreamSynchronize(ctx->stream));
     const int W = kf->W;
-    for (const Band& b : kf->bands) {  // each band's own rows
+    int inliers = 0;
+    for (Band& b : kf->bands) {  // each local band's own rows
+      if (!b.local) continue;
       const long o = (long)b.y0 * W;
       const size_t n = (size_t)(b.y1 - b.y0) * W;
       auto cp = [&](void* dst, const void* src, size_t elem) {
@@ -426,12 +563,14 @@ int dfuse_bkf_download(dfuse_banded_keyframe* kf, double* log_depth, double* sca
       cp(semi_depth, b.semi_d, sizeof(double));
       cp(semi_variance, b.semi_v, sizeof(double));
       cp(semi_valid, b.semi_valid, 1);
+      DF_CUDA(cudaMemcpyAsync(b.h_counters, b.counters + 2, 2 * sizeof(int),
+                              cudaMemcpyDeviceToHost, ctx->stream));
     }
-    if (inlier_count)
-      DF_CUDA(cudaMemcpyAsync(inlier_count, kf->shared + 1, sizeof(int), cudaMemcpyDeviceToHost,
-                              ctx->stream));
     if (mask) DF_CUDA(cudaMemcpyAsync(mask, kf->mask, kf->P, cudaMemcpyDeviceToHost, ctx->stream));
     DF_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (Band& b : kf->bands)
+      if (b.local) inliers += b.h_counters[1];
+    if (inlier_count) *inlier_count = inliers;
     if (scale) *scale = st.scale;
     if (iteration) *iteration = st.iteration;
   });

@@ -1235,7 +1235,16 @@ __global__ void __launch_bounds__(FT, 1) k_fusion_banded(BandLaunch L) {
     __syncthreads();
   }
   sweep_prologue(a, rg);
-  grid_sync(c);  // fenced: the per-call planes (and their halo rows) are read at i-1, i-W
+  // fenced (the per-call planes and their halo rows are read at i-1, i-W),
+  // and the inlier count of the whole keyframe: each band holds its own
+  double v[1] = {c.me == 0 && threadIdx.x == 0 ? (double)*a.inlier_dev : 0.0};
+  grid_allreduce(c, v);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_args.inlier_count = (int)v[0];
+    s_args.inlier_dev = nullptr;
+  }
+  __syncthreads();
   int status = 0;
   optimize_body<0, 0>(c, a, rg, sel, leader, status);
   if (leader) {
@@ -1245,10 +1254,11 @@ __global__ void __launch_bounds__(FT, 1) k_fusion_banded(BandLaunch L) {
 }
 
 void launch_fusion_banded(dfuse_ctx* ctx, const FusionArgs* args_dev,
-                          unsigned long long* const* rank_slots_dev, int nband, int cpr) {
-  BandLaunch L{args_dev, rank_slots_dev, nband, cpr, 0, 0};
+                          unsigned long long* const* rank_slots_dev, int nband, int cpr,
+                          int band0, int nlocal, int sys) {
+  BandLaunch L{args_dev, rank_slots_dev, nband, cpr, band0, sys};
   void* argv[] = {&L};
-  DF_CUDA(cudaLaunchCooperativeKernel((const void*)k_fusion_banded, dim3(nband * cpr), dim3(FT),
+  DF_CUDA(cudaLaunchCooperativeKernel((const void*)k_fusion_banded, dim3(nlocal * cpr), dim3(FT),
                                       argv, 0, ctx->stream));
   DF_LAUNCHED(ctx);
 }

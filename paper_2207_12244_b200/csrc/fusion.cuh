@@ -98,8 +98,10 @@ void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid);
 void launch_gradient(dfuse_ctx* ctx, FusionArgs& a, int grid, double* g);
 // row-band optimize: args_dev[nband] (device), one cooperative launch of
 // nband * cpr CTAs (fusion.cu, k_fusion_banded)
+// (bands band0 .. band0 + nlocal - 1 of nband; sys: bands on several GPUs)
 void launch_fusion_banded(dfuse_ctx* ctx, const FusionArgs* args_dev,
-                          unsigned long long* const* rank_slots_dev, int nband, int cpr);
+                          unsigned long long* const* rank_slots_dev, int nband, int cpr,
+                          int band0, int nlocal, int sys);
 size_t band_rank_slots_bytes(int nband);
 void launch_stencil_apply(dfuse_ctx* ctx, int W, int H, const double* diag, const double* right,
                           const double* down, const double* x, double* y);

@@ -41,13 +41,22 @@ def _free_port():
 def _worker(rank, world, port, q):
     import torch.distributed as dist
 
+    from paper_2207_12244_b200 import bands_dist
+
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     mine = shard.keyframes_for_rank(64, world, rank)
     t = shard.max_over_ranks(10.0 + rank)
+    # row-band peer exchange (bands_dist): every rank gets every record, in
+    # rank order, byte for byte; band counts are summed over ranks
+    r0, r1 = shard.row_bands(2160, world)[rank]
+    me = bands_dist.BandPeer(bytes([rank + 1]) * 64, 148 - rank, r0, r1, 3840)
+    recs = bands_dist.exchange_peers(bytes(me), world)
+    peers = [bands_dist.BandPeer.from_buffer_copy(r) for r in recs]
+    counts = bands_dist.sum_over_ranks([100 + rank, 7 * rank], world)
     dist.barrier()
-    q.put((rank, mine, t))
+    q.put((rank, mine, t, [(p.handle[0], p.cpr, p.y0, p.y1, p.width) for p in peers], counts))
     dist.destroy_process_group()
 
 
@@ -64,3 +73,7 @@ def test_two_rank_gloo():
         assert p.exitcode == 0
     assert res[0][2] == res[1][2] == 11.0
     assert sorted(res[0][1] + res[1][1]) == list(range(64))
+    bands = shard.row_bands(2160, 2)
+    expect = [(g + 1, 148 - g, bands[g][0], bands[g][1], 3840) for g in range(2)]
+    assert res[0][3] == res[1][3] == expect
+    assert res[0][4] == res[1][4] == [201, 7]

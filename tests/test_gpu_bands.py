@@ -89,3 +89,27 @@ def test_band_count_is_validated(gpu_ctx):
         api.BandedKeyframe(gpu_ctx, spec.camera(), seq.I0, seq.pred, 9, 0.02)
     with pytest.raises(Exception):
         api.BandedKeyframe(gpu_ctx, spec.camera(), seq.I0, seq.pred, 0, 0.02)
+
+
+def test_rank_form_single_process(gpu_ctx):
+    """dfuse_bkf_create_rank with world 1 (no peers to connect): the same
+    band, the same kernel with system-scope fences, the same bits as the
+    single-launch form."""
+    from paper_2207_12244_b200.bands_dist import DistributedBandedKeyframe
+
+    spec = synth.small_spec(160, 120, frames=2)
+    seq = synth.make_sequence(spec, 12, frames=2)
+    cfg = RobustConfig(gn_iterations=4)
+    a = api.BandedKeyframe(gpu_ctx, spec.camera(), seq.I0, seq.pred, 1, 0.02)
+    b = DistributedBandedKeyframe(gpu_ctx, spec.camera(), seq.I0, seq.pred, 0.02, world=1, rank=0)
+    for q, t, I1 in seq.frames:
+        g = _geom(gpu_ctx, spec, q, t)
+        ra = a.process_frame(g, I1, spec.search, cfg, "full")
+        rb = b.process_frame(g, I1, spec.search, cfg, "full")
+        assert (ra.observations, ra.inlier_count) == (rb.observations, rb.inlier_count)
+    sa, ma, _ = a.download()
+    sb, mb, _ = b.download()
+    assert sa.log_depth.tobytes() == sb.log_depth.tobytes()
+    assert ma.depth.tobytes() == mb.depth.tobytes() and ma.inlier_count == mb.inlier_count
+    a.close()
+    b.close()
