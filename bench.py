@@ -57,6 +57,11 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--bands", type=int, default=0,
+                    help="row bands of one keyframe (C4 form); under torchrun with --config C4 "
+                         "each rank computes one band (strong scaling)")
+    ap.add_argument("--frames", type=int, default=0,
+                    help="tracked frames to generate (default: the config's)")
     ap.add_argument("--solver-path", default="auto",
                     choices=["auto", "resident", "resident1r", "resident2r", "streaming"],
                     help="PCG data path (dfuse_ctx_set_solver_path); auto is the product default")
@@ -278,11 +283,26 @@ def main():
     from paper_2207_12244_b200 import api
     from paper_2207_12244_b200._ffi import SemiDenseMap
 
-    seq = synth.make_sequence(spec, args.seed + 1000 * rank)
+    # C4 under torchrun: ONE keyframe split into row bands across the ranks
+    # (strong scaling); otherwise every rank runs its own keyframe stream
+    # (C2/C3 form, weak scaling)
+    split = args.config == "C4" and ws > 1
+    seq = synth.make_sequence(spec, args.seed + (0 if split else 1000 * rank),
+                              frames=args.frames or None)
     cfg = solver_cfg(spec, args.regime)
     ctx = api.context(device)
     ctx.set_solver_path(args.solver_path)
-    kf = api.Keyframe(ctx, spec.camera(), seq.I0, seq.pred, 0.02)
+    if split:
+        from paper_2207_12244_b200.bands_dist import DistributedBandedKeyframe
+
+        kf = DistributedBandedKeyframe(ctx, spec.camera(), seq.I0, seq.pred, 0.02)
+    elif args.bands > 0:
+        kf = api.BandedKeyframe(ctx, spec.camera(), seq.I0, seq.pred, args.bands, 0.02)
+    else:
+        kf = api.Keyframe(ctx, spec.camera(), seq.I0, seq.pred, 0.02)
+    download = (api.lib().dfuse_bkf_download if isinstance(kf, api.BandedKeyframe)
+                else api.lib().dfuse_kf_download)
+    jobs = 1 if split else ws  # keyframe updates per step, whole job
     geoms = [ctx.api.make_epipolar_geometry(synth.IDENTITY_Q, np.zeros(3), q, t, spec.camera())
              for (q, t, _) in seq.frames]
     dev_frames = [torch.from_numpy(np.ascontiguousarray(I1, np.float32)).cuda(device)
@@ -340,7 +360,7 @@ def main():
         t = torch.tensor([total_ms], device=f"cuda:{device}", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
-    value = ws * args.steps / (total_ms / 1e3)
+    value = jobs * args.steps / (total_ms / 1e3)
 
     # ---------------- end-to-end through the C-ABI with host buffers
     e2e = None
@@ -356,14 +376,13 @@ def main():
         t0 = time.perf_counter()
         for _ in range(args.steps):
             step(dev=False, host_images=host_imgs)
-            api.lib().dfuse_kf_download(kf.handle, out_ld.ctypes.data, None, None, None, None,
-                                        None, None, None)
+            download(kf.handle, out_ld.ctypes.data, None, None, None, None, None, None, None)
         dt = time.perf_counter() - t0
         if ws > 1:
             t = torch.tensor([dt], device=f"cuda:{device}", dtype=torch.float64)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             dt = float(t.item())
-        e2e = {"value": round(ws * args.steps / dt, 4), "unit": UNIT,
+        e2e = {"value": round(jobs * args.steps / dt, 4), "unit": UNIT,
                "h2d_bytes_per_step": int(P * 4),
                "d2h_bytes_per_step": int(P * 8 + C.sizeof(api.FrameResultC))}
 
@@ -378,14 +397,18 @@ def main():
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded Perlin-textured planes; BASELINE C2 shapes/distributions)",
+        "scaling": "strong" if split else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (seeded Perlin-textured planes; BASELINE {spec.name} "
+                "shapes/distributions)",
         "config": {"workload": f"{spec.name}: {spec.width}x{spec.height} keyframe, {nF} tracked "
                                f"frames (reset after the last), solver {args.regime}",
                    "regime": args.regime, "solver_path": args.solver_path,
                    "gn_iterations": cfg.gn_iterations,
                    "cg_tol": cfg.cg_tol, "cg_max_iters": cfg.cg_max_iters,
-                   "parallelism": f"replicas x{ws} (independent keyframes)",
+                   "parallelism": (f"row bands x{ws} (one keyframe; halo rows and the "
+                                   "band-level all-reduce over NVLink peer memory)") if split
+                   else (f"replicas x{ws} (independent keyframes)"
+                         + (f", {args.bands} row bands each" if args.bands else "")),
                    "l2": "flushed before every step (512 MiB write)"},
         "mpix_per_s": round(value * P / 1e6, 4),
         "stage_ms": {"stereo": round(float(np.mean(stereo_ms)), 4),

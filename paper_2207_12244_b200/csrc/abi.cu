@@ -121,7 +121,7 @@ struct FusionWS {
   double* irs;
   double* ivar[3];
   double* ld[2];
-  double *diag, *right, *down, *b, *x, *r, *p0, *p1, *q;
+  double *diag, *right, *down, *b, *x, *r, *z, *p0, *p1, *q;
   ReduceSlot* slots;
   unsigned long long* halo;
   FusionControl* ctl;
@@ -133,7 +133,7 @@ size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 FusionWS alloc_fusion_ws(dfuse_ctx* ctx, long P, int grid, int slot) {
   const size_t dP = align_up(sizeof(double) * P);
   const bool resident = fusion_resident_possible(P, grid);
-  size_t total = 6 * dP + 7 * dP + align_up(P) + 11 * dP + align_up(fusion_slots_bytes(grid)) +
+  size_t total = 6 * dP + 7 * dP + align_up(P) + 12 * dP + align_up(fusion_slots_bytes(grid)) +
                  align_up(sizeof(FusionControl)) + align_up(2 * sizeof(FusionStateDev)) +
                  (resident ? align_up(fusion_halo_bytes(P)) : 0);
   char* base = (char*)scratch(ctx, slot, total);
@@ -159,6 +159,7 @@ FusionWS alloc_fusion_ws(dfuse_ctx* ctx, long P, int grid, int slot) {
   w.b = (double*)take(dP);
   w.x = (double*)take(dP);
   w.r = (double*)take(dP);
+  w.z = (double*)take(dP);
   w.p0 = (double*)take(dP);
   w.p1 = (double*)take(dP);
   w.q = (double*)take(dP);
@@ -189,6 +190,7 @@ void fill_args(FusionArgs& a, const FusionWS& w, int W, int H) {
   a.b = w.b;
   a.x = w.x;
   a.r = w.r;
+  a.z = w.z;
   a.p[0] = w.p0;
   a.p[1] = w.p1;
   a.q = w.q;

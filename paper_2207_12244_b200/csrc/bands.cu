@@ -29,11 +29,11 @@ namespace {
 
 size_t al(size_t v) { return (v + 255) & ~size_t(255); }
 
-enum BandPlane {  // the 24 double planes of a band, in allocation order
+enum BandPlane {  // the 25 double planes of a band, in allocation order
   BP_PRED0 = 0, BP_SD = 6, BP_SV, BP_LNSD, BP_IRS, BP_IV0, BP_IV1, BP_IV2, BP_LD0, BP_LD1,
-  BP_DIAG, BP_RIGHT, BP_DOWN, BP_B, BP_X, BP_R, BP_P0, BP_P1, BP_Q, BP_COUNT
+  BP_DIAG, BP_RIGHT, BP_DOWN, BP_B, BP_X, BP_R, BP_Z, BP_P0, BP_P1, BP_Q, BP_COUNT
 };
-static_assert(BP_COUNT == 24, "plane count");
+static_assert(BP_COUNT == 25, "plane count");
 
 struct Band {
   int y0 = 0, y1 = 0;
@@ -50,7 +50,7 @@ struct Band {
   FusionStateDev* st = nullptr;  // [2]
   BandNb* nb_dev = nullptr;
   FusionArgs fa;  // device pointers, shifted to global pixel indices
-  double* plane_base[24];  // unshifted plane starts (for copies)
+  double* plane_base[BP_COUNT];  // unshifted plane starts (for copies)
 };
 
 }  // namespace
@@ -164,6 +164,7 @@ void bind_band(dfuse_banded_keyframe* kf, Band& b, char* base, int cpr) {
   f.b = sh[BP_B];
   f.x = sh[BP_X];
   f.r = sh[BP_R];
+  f.z = sh[BP_Z];
   f.p[0] = sh[BP_P0];
   f.p[1] = sh[BP_P1];
   f.q = sh[BP_Q];
@@ -196,8 +197,7 @@ BandNb neighbours(dfuse_banded_keyframe* kf, int g) {
     out[HP_LD0] = f.ld[0];
     out[HP_LD1] = f.ld[1];
     out[HP_X] = f.x;
-    out[HP_R] = f.r;
-    out[HP_DIAG] = f.diag;
+    out[HP_Z] = f.z;
     out[HP_DOWN] = f.down;
     out[HP_P0] = f.p[0];
     out[HP_P1] = f.p[1];

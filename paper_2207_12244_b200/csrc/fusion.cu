@@ -688,8 +688,8 @@ __device__ __forceinline__ void sweep_assemble_body(
     const Range rg, const int W, const int H, const Sel sel, const double dnet, const double dsemi,
     const double dgrad, const double* __restrict__ ld, const double ln_s, const SweepPlanes pl,
     double* __restrict__ o_diag, double* __restrict__ o_right, double* __restrict__ o_down,
-    double* __restrict__ o_r, double* __restrict__ o_b, double (&v)[4], const BandNb* nb,
-    const int y0, const int y1) {
+    double* __restrict__ o_r, double* __restrict__ o_b, double* __restrict__ o_z, double (&v)[4],
+    const BandNb* nb, const int y0, const int y1) {
   double bn = 0.0, rz = 0.0, bad = 0.0, cost = 0.0;
   for (int i0 = rg.beg + threadIdx.x; i0 < rg.end; i0 += U * FT) {
 #pragma unroll
@@ -755,13 +755,16 @@ __device__ __forceinline__ void sweep_assemble_body(
         o_right[i] = right;
         o_down[i] = down;
         o_r[i] = b;
-        halo_put(nb, y0, y1, HP_DIAG, i, y, diag);
         halo_put(nb, y0, y1, HP_DOWN, i, y, down);
-        halo_put(nb, y0, y1, HP_R, i, y, b);
         if (o_b) o_b[i] = b;
+        const double z = b / diag;  // PCG init z = r/diag, fusion.hpp:329
+        if (o_z) {
+          o_z[i] = z;
+          halo_put(nb, y0, y1, HP_Z, i, y, z);
+        }
         bn += b * b;
         if (!(diag > 0.0)) bad += 1.0;
-        rz += b * (b / diag);
+        rz += b * z;
         cost += c;
       }
     }
@@ -776,7 +779,7 @@ template <int U>
 __device__ void sweep_assemble(const FusionArgs& a, const Sel& sel, const Range& rg,
                                const double* ld, double ln_s, bool store_b, double (&v)[4]) {
   sweep_assemble_body<U>(rg, a.W, a.H, sel, a.dnet, a.dsemi, a.dgrad, ld, ln_s, planes_of(a),
-                         a.diag, a.right, a.down, a.r, store_b ? a.b : nullptr, v, a.nb,
+                         a.diag, a.right, a.down, a.r, store_b ? a.b : nullptr, a.z, v, a.nb,
                          a.band_y0, a.band_y1);
 }
 
@@ -786,9 +789,11 @@ __device__ void sweep_pcg_init(const FusionArgs& a, const Range& rg, double (&v)
   for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) {
     const double b = a.b[i], d = a.diag[i];
     a.r[i] = b;
+    const double z = b / d;  // fusion.hpp:329
+    if (a.z) a.z[i] = z;
     bn += b * b;
     if (!(d > 0.0)) bad += 1.0;
-    rz += b * (b / d);
+    rz += b * z;
   }
   v[0] = bn;
   v[1] = rz;
@@ -804,61 +809,108 @@ __device__ void sweep_zero_x(const FusionArgs& a, const Range& rg) {
 }
 
 // ---------------------------------------------------------------------------
-// streaming PCG
-// p at pixel j for iteration it: z_j + beta p_prev_j (fusion.hpp:360,365);
-// at it == 0, p = z (fusion.hpp:329-330)
-__device__ __forceinline__ double p_at(const FusionArgs& a, const double* pprev, double beta,
-                                       bool first, int j) {
-  const double z = a.r[j] / a.diag[j];
-  return first ? z : z + beta * pprev[j];
-}
+// streaming PCG (rasters too large for the SM-resident tiles, e.g. C4's 4K).
+// z = r/diag is stored by the sweep that updates r (one IEEE division per
+// pixel, fusion.hpp:329,359), so sweep A rebuilds p at the four neighbours
+// from (z, p_prev) alone. Both sweeps are written like the Gauss-Newton
+// sweeps: unrolled predicated pixel groups, unconditional clamped loads,
+// skipped stencil terms removed by selects, __restrict__ planes.
 
-// sweep A: q = H p (StencilMatrix::apply order, fusion.hpp:127-132), p.q
-__device__ double sweep_pcg_a(const FusionArgs& a, const Range& rg, int it, double beta) {
-  const double* pprev = a.p[(it + 1) & 1];
-  double* pcur = a.p[it & 1];
-  const bool first = it == 0;
-  const int W = a.W, H = a.H;
+// sweep A: p = z + beta p_prev (p = z at it 0, fusion.hpp:329-330,364),
+// q = H p in StencilMatrix::apply order (fusion.hpp:127-132); returns p.q
+template <int U, bool FIRST>
+__device__ __forceinline__ double sweep_pcg_a_body(
+    const Range rg, const int W, const int H, const double beta, const double* __restrict__ z,
+    const double* __restrict__ pprev, const double* __restrict__ diag,
+    const double* __restrict__ right, const double* __restrict__ down, double* __restrict__ pcur,
+    double* __restrict__ q, const BandNb* nb, const int y0, const int y1, const int pplane) {
   double pq = 0.0;
-  for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) {
-    const int y = i / W, x = i - y * W;
-    const double pi = p_at(a, pprev, beta, first, i);
-    double v = a.diag[i] * pi;
-    if (x + 1 < W) v += a.right[i] * p_at(a, pprev, beta, first, i + 1);
-    if (x > 0) v += a.right[i - 1] * p_at(a, pprev, beta, first, i - 1);
-    if (y + 1 < H) v += a.down[i] * p_at(a, pprev, beta, first, i + W);
-    if (y > 0) v += a.down[i - W] * p_at(a, pprev, beta, first, i - W);
-    pcur[i] = pi;
-    halo_put(a, (it & 1) ? HP_P1 : HP_P0, i, pi);
-    a.q[i] = v;
-    pq += pi * v;
+  for (int i0 = rg.beg + threadIdx.x; i0 < rg.end; i0 += U * FT) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int iu = i0 + u * FT;
+      const bool in = iu < rg.end;
+      const int i = in ? iu : rg.beg;
+      const int y = i / W, x = i - y * W;
+      const bool hr = x + 1 < W, hl = x > 0, hd = y + 1 < H, hu = y > 0;
+      const int jr = hr ? i + 1 : i, jl = hl ? i - 1 : i, jd = hd ? i + W : i, ju = hu ? i - W : i;
+      const double pc = FIRST ? z[i] : z[i] + beta * pprev[i];
+      const double pr = FIRST ? z[jr] : z[jr] + beta * pprev[jr];
+      const double pl = FIRST ? z[jl] : z[jl] + beta * pprev[jl];
+      const double pd = FIRST ? z[jd] : z[jd] + beta * pprev[jd];
+      const double pu = FIRST ? z[ju] : z[ju] + beta * pprev[ju];
+      const double tr = right[i] * pr, tl = right[jl] * pl, td = down[i] * pd, tu = down[ju] * pu;
+      double v = diag[i] * pc;
+      v += hr ? tr : 0.0;
+      v += hl ? tl : 0.0;
+      v += hd ? td : 0.0;
+      v += hu ? tu : 0.0;
+      if (in) {
+        pcur[i] = pc;
+        halo_put(nb, y0, y1, pplane, i, y, pc);
+        q[i] = v;
+        pq += pc * v;
+      }
+    }
   }
   return pq;
 }
 
-// sweep B (fusion.hpp:345-362): returns (r.r, r.z)
-__device__ void sweep_pcg_b(const FusionArgs& a, const Range& rg, int it, double alpha,
-                            double (&v)[2]) {
-  const double* pcur = a.p[it & 1];
+template <int U>
+__device__ double sweep_pcg_a(const FusionArgs& a, const Range& rg, int it, double beta) {
+  const int pplane = (it & 1) ? HP_P1 : HP_P0;
+  if (it == 0)
+    return sweep_pcg_a_body<U, true>(rg, a.W, a.H, beta, a.z, a.p[(it + 1) & 1], a.diag, a.right,
+                                     a.down, a.p[it & 1], a.q, a.nb, a.band_y0, a.band_y1, pplane);
+  return sweep_pcg_a_body<U, false>(rg, a.W, a.H, beta, a.z, a.p[(it + 1) & 1], a.diag, a.right,
+                                    a.down, a.p[it & 1], a.q, a.nb, a.band_y0, a.band_y1, pplane);
+}
+
+// sweep B (fusion.hpp:345-362): x += alpha p, r -= alpha q, z = r/diag;
+// returns (r.r, r.z)
+template <int U>
+__device__ __forceinline__ void sweep_pcg_b_body(
+    const Range rg, const int W, const bool first, const double alpha,
+    const double* __restrict__ pcur, const double* __restrict__ q, const double* __restrict__ diag,
+    double* __restrict__ x, double* __restrict__ r, double* __restrict__ z, const BandNb* nb,
+    const int y0, const int y1, double (&v)[2]) {
   double rr = 0.0, rz = 0.0;
-  for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) {
-    const double xo = it == 0 ? 0.0 : a.x[i];
-    const double xn = xo + alpha * pcur[i];
-    a.x[i] = xn;
-    halo_put(a, HP_X, i, xn);
-    const double r = a.r[i] - alpha * a.q[i];
-    a.r[i] = r;
-    halo_put(a, HP_R, i, r);
-    rr += r * r;
-    rz += r * (r / a.diag[i]);
+  for (int i0 = rg.beg + threadIdx.x; i0 < rg.end; i0 += U * FT) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int iu = i0 + u * FT;
+      const bool in = iu < rg.end;
+      const int i = in ? iu : rg.beg;
+      const double xo = first ? 0.0 : x[i];
+      const double xn = xo + alpha * pcur[i];
+      const double rn = r[i] - alpha * q[i];
+      const double zn = rn / diag[i];
+      if (in) {
+        const int y = i / W;
+        x[i] = xn;
+        r[i] = rn;
+        z[i] = zn;
+        halo_put(nb, y0, y1, HP_X, i, y, xn);
+        halo_put(nb, y0, y1, HP_Z, i, y, zn);
+        rr += rn * rn;
+        rz += rn * zn;
+      }
+    }
   }
   v[0] = rr;
   v[1] = rz;
 }
 
+template <int U>
+__device__ void sweep_pcg_b(const FusionArgs& a, const Range& rg, int it, double alpha,
+                            double (&v)[2]) {
+  sweep_pcg_b_body<U>(rg, a.W, it == 0, alpha, a.p[it & 1], a.q, a.diag, a.x, a.r, a.z, a.nb,
+                      a.band_y0, a.band_y1, v);
+}
+
 // Jacobi PCG after init (solve_depth_step, fusion.hpp:334-367). Returns the
 // error code (0 ok); *its = iterations run.
-template <class Ctx>
+template <int SU, class Ctx>
 __device__ int pcg_stream(Ctx& c, const FusionArgs& a, const Range& rg, double bnorm2,
                           double rz, int* its) {
   const double tol2 = a.cg_tol * a.cg_tol * bnorm2;
@@ -868,12 +920,12 @@ __device__ int pcg_stream(Ctx& c, const FusionArgs& a, const Range& rg, double b
   *its = 0;
   for (int it = 0; it < a.cg_max; ++it) {
     *its = it + 1;
-    double v1[1] = {sweep_pcg_a(a, rg, it, beta)};
+    double v1[1] = {sweep_pcg_a<SU>(a, rg, it, beta)};
     grid_allreduce(c, v1);
     if (!(v1[0] > 0.0)) return DFUSE_E_CG_DIVERGENCE;
     const double alpha = rz / v1[0];
     double v2[2];
-    sweep_pcg_b(a, rg, it, alpha, v2);
+    sweep_pcg_b<SU>(a, rg, it, alpha, v2);
     grid_allreduce(c, v2);
     const double rn = v2[0];
     if (rn <= tol2) return 0;
@@ -921,7 +973,7 @@ __device__ __forceinline__ int pcg_solve(Ctx& c, const FusionArgs& a, const Rang
     const int st = pcg_resident_pipe<PPT>(c, a, bnorm2, rz, its, &h);
     return st >= 0 ? st : pcg_resume_cg<PPT>(c, a, bnorm2, h, its);
   } else {
-    const int st = pcg_stream(c, a, rg, bnorm2, rz, its);
+    const int st = pcg_stream<4>(c, a, rg, bnorm2, rz, its);
     if (*its == 0) {
       sweep_zero_x(a, rg);
       grid_sync(c);

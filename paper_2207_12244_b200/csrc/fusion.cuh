@@ -39,9 +39,7 @@ struct FusionControl {
 // indices address them; the planes read at i - W / i + W get their halo row
 // from the neighbour band, which writes its boundary row into both its own
 // plane and ours (a remote store when bands live on different GPUs).
-enum HaloPlane {
-  HP_LD0, HP_LD1, HP_X, HP_R, HP_DIAG, HP_DOWN, HP_P0, HP_P1, HP_IV2, HP_COUNT
-};
+enum HaloPlane { HP_LD0, HP_LD1, HP_X, HP_Z, HP_DOWN, HP_P0, HP_P1, HP_IV2, HP_COUNT };
 struct BandNb {
   double* up[HP_COUNT];  // the band above's plane (whose bottom halo row is our row y0), or null
   double* dn[HP_COUNT];  // the band below's plane (whose top halo row is our row y1 - 1), or null
@@ -72,6 +70,7 @@ struct FusionArgs {
   double* b;
   double* x;
   double* r;
+  double* z;  // streaming PCG: z = r/diag (null: the resident path keeps z on chip)
   double* p[2];
   double* q;
   ReduceSlot* slots;  // [2][grid] all-reduce slots (+1)

@@ -161,7 +161,7 @@ void kf_alloc(dfuse_keyframe* kf, const dfuse_intrinsics* K) {
   const size_t dP = al(sizeof(double) * P);
   const bool resident = fusion_resident_possible(P, kf->grid);
   const size_t total = 2 * al(sizeof(float) * P) + al(P) + al(sizeof(int) * P) + 2 * dP +
-                       al(P) + 256 + 11 * dP + 11 * dP + al(fusion_slots_bytes(kf->grid)) +
+                       al(P) + 256 + 11 * dP + 12 * dP + al(fusion_slots_bytes(kf->grid)) +
                        al(sizeof(FusionControl)) + al(2 * sizeof(FusionStateDev)) +
                        (resident ? al(fusion_halo_bytes(P)) : 0);
   DF_CUDA(cudaMalloc(&kf->block, total));
@@ -199,6 +199,7 @@ void kf_alloc(dfuse_keyframe* kf, const dfuse_intrinsics* K) {
   f.b = (double*)take(dP);
   f.x = (double*)take(dP);
   f.r = (double*)take(dP);
+  f.z = (double*)take(dP);
   f.p[0] = (double*)take(dP);
   f.p[1] = (double*)take(dP);
   f.q = (double*)take(dP);
