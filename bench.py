@@ -419,7 +419,11 @@ def main():
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": ncu_traffic("k_fusion"),
                      "traffic_source": "profiles/ncu_traffic.json (ncu --set full, one launch)",
-                     "bytes_per_update": float(np.mean(fusion_bytes))},
+                     "bytes_per_update": float(np.mean(fusion_bytes)),
+                     "note": "achieved = SURVEY 8(d) streaming byte model (351 + 112 n_cg B/px "
+                             "per GN step, executed counts) / k_fusion device time; the "
+                             "SM-resident solver moves only `traffic` DRAM bytes per launch, so "
+                             "frac > 1 = faster than a streaming solver at full HBM bandwidth"},
         "gpu_launches": int(launches),
         "clocks": clocks,
         "e2e": e2e,
