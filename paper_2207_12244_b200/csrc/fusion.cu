@@ -48,8 +48,11 @@
 #include "fusion.cuh"
 
 namespace dfuse_cuda {
+#ifndef DFUSE_FT
+#define DFUSE_FT 512
+#endif
 
-constexpr int FT = 512;  // threads per CTA (one CTA per SM)
+constexpr int FT = DFUSE_FT;  // threads per CTA (one CTA per SM)
 constexpr int FW = FT / 32;
 
 struct Sel {
