@@ -994,14 +994,16 @@ __device__ __forceinline__ void optimize_body(Ctx& c, const FusionArgs& a, const
                                               const Sel& sel, const bool leader, int& status) {
   constexpr int SU = PPT > 0 ? PPT : 2;  // pixels per thread per unrolled sweep group
   FusionControl* ctl = a.ctl;
-  const FusionStateDev st0 = *a.st_in;
-  double scale = st0.scale;
-  int iteration = st0.iteration;
-  int cur = st0.cur;
+  // State that lives across the PCG call sits in shared memory where it can,
+  // so the (inlined) PCG loop keeps the register file: the counters (thread
+  // 0 only) and the input state (re-read at the end).
+  __shared__ int gn_cnt[3];     // cost_evals, pcg_total, gn_done
+  double scale = a.st_in->scale;
+  int cur = a.st_in->cur;
   const int inliers = a.inlier_dev ? *a.inlier_dev : a.inlier_count;
   const bool ls_mode = a.mode == DFUSE_MODE_LSSCALE;
   const bool depth_solvable = !ls_mode || inliers > 0;
-  int cost_evals = 0, pcg_total = 0, gn_done = 0;
+  if (threadIdx.x == 0) gn_cnt[0] = gn_cnt[1] = gn_cnt[2] = 0;
   const bool otr = a.trace && leader;  // DFUSE_TRACE: ns per GN phase, CTA 0
   __shared__ long long ot[8];          // [7] = last timestamp (thread 0 only)
   if (otr)
@@ -1012,16 +1014,17 @@ if (otr) {                        \
   ot[k] += t_ - ot[7];            \
   ot[7] = t_;                     \
 }
+  const bool scale_block = !ls_mode && a.est_scale && inliers > 0;  // fusion.hpp:411
+  extern __shared__ double dsm_stage[];
+  double* stage = a.stage_n > 0 ? dsm_stage : nullptr;
   for (int it = 0; it < a.gn && status == 0; ++it) {
     if (otr) ot[7] = df_now();
     bool have_eq = false;  // the scale block left an assembly valid for the depth block
     double veq[4] = {0.0, 0.0, 0.0, 0.0};
-    if (!ls_mode && a.est_scale && inliers > 0) {  // fusion.hpp:411-425
+    if (scale_block) {  // fusion.hpp:411-425
       const double ln_s0 = log(scale);
       double ln_s = ln_s0;
       double c0 = 0.0;
-      extern __shared__ double dsm_stage[];
-      double* stage = a.stage_n > 0 ? dsm_stage : nullptr;
       // the scale sweeps write no global memory, so their all-reduces need
       // no fence
       for (int round = 0; round < 3; ++round) {
@@ -1047,7 +1050,7 @@ if (otr) {                        \
           ln_s = w[0] / w[1];
         }
       }
-      cost_evals += 1;
+      if (threadIdx.x == 0) gn_cnt[0] += 1;
       DF_OTRACE(0);
       const double s_new = exp(ln_s);
       const double dlns = log(s_new) - log(scale);
@@ -1076,7 +1079,7 @@ if (otr) {                        \
           grid_allreduce<1, false>(c, v);
           tc = v[0];
         }
-        cost_evals += 1;
+        if (threadIdx.x == 0) gn_cnt[0] += 1;
         if (tc <= c0) {
           scale = ts;
           accepted = step;
@@ -1097,7 +1100,7 @@ if (otr) {                        \
         grid_allreduce(c, v);
       }
       const double c0 = v[3];
-      cost_evals += 1;
+      if (threadIdx.x == 0) gn_cnt[0] += 1;
       DF_OTRACE(2);
       int its = 0;
       if (v[0] != 0.0) {
@@ -1108,7 +1111,7 @@ if (otr) {                        \
         }
       }
       DF_OTRACE(3);
-      pcg_total += its;
+      if (threadIdx.x == 0) gn_cnt[1] += its;
       if (leader && it < DFUSE_STATS_MAX_GN) ctl->stats.pcg_iters[it] = its;
       if (status) break;
       double step = 1.0, accepted = 0.0;
@@ -1121,7 +1124,7 @@ if (otr) {                        \
           w[0] = sweep_cost<SU>(a, sel, rg, TrialLd{a.ld[cur], a.x, step}, ln_s, a.ld[1 - cur]);
         DF_OTRACE(6);
         grid_allreduce(c, w);
-        cost_evals += 1;
+        if (threadIdx.x == 0) gn_cnt[0] += 1;
         if (w[0] <= c0) {
           cur = 1 - cur;
           accepted = step;
@@ -1132,8 +1135,7 @@ if (otr) {                        \
       if (leader && it < DFUSE_STATS_MAX_GN) ctl->stats.depth_step[it] = accepted;
       DF_OTRACE(4);
     }
-    iteration += 1;
-    gn_done = it + 1;
+    if (threadIdx.x == 0) gn_cnt[2] = it + 1;  // gn_done; iteration += 1 (fusion.hpp:442)
   }
 #undef DF_OTRACE
   if (otr)
@@ -1152,19 +1154,19 @@ if (otr) {                        \
     scale = exp(offset);
   }
   if (leader) {
-    FusionStateDev out = st0;  // transactional: unchanged on error
+    FusionStateDev out = *a.st_in;  // transactional: unchanged on error
     if (status == 0) {
       out.scale = scale;
-      out.iteration = iteration;
+      out.iteration += gn_cnt[2];
       out.cur = cur;
     }
     *a.st_out = out;
     ctl->scale = out.scale;
     ctl->iteration = out.iteration;
     ctl->ld_final = out.cur;
-    ctl->stats.gn_done = gn_done;
-    ctl->stats.pcg_total = pcg_total;
-    ctl->stats.cost_evals = cost_evals;
+    ctl->stats.gn_done = gn_cnt[2];
+    ctl->stats.pcg_total = gn_cnt[1];
+    ctl->stats.cost_evals = gn_cnt[0];
   }
 }
 
