@@ -1,42 +1,7 @@
-// fusion.cu -- the probabilistic fusion optimiser on sm_100a.
-//
-// One persistent, cooperatively launched kernel (k_fusion) runs a whole
-// optimize() call (fusion.hpp:402-454) on the device with no host round
-// trips: the alternating scale / depth Gauss-Newton iterations, the Huber
-// IRLS weights, the line searches and the Jacobi-PCG loop
-// (fusion.hpp:316-368). The reductions the reference performs sequentially
-// are deterministic trees (warp butterfly -> CTA -> fixed-order sum over the
-// per-CTA partials); each ends in a grid-wide exchange after which every CTA
-// holds the same bits and takes the same control decision.
-//
-// Sweeps over the raster (each CTA owns a contiguous pixel range), each
-// followed by exactly one grid all-reduce:
-//   scale round 0  : Huber-weighted (num, den) of the scale IRLS + the
-//                    scale block's c0 = total_cost(st)       fusion.hpp:378-389,413
-//   scale rounds 1,2
-//   scale trial    : total_cost at exp(ln s + step dlns)     fusion.hpp:416-424
-//   assemble       : gather-form normal equations + b.b + r.z + diag>0 check
-//                    + the depth block's c0                  fusion.hpp:171-222,319-332,429
-//   depth trial    : trial = st + step delta (written to the other ld
-//                    buffer; accepted = pointer swap), cost  fusion.hpp:430-440
-// PCG (fusion.hpp:338-366), two paths:
-//   resident  (raster fits on chip, e.g. 640x480 on 148 SMs): CTA b owns
-//             tile b; x, r, z stay in registers, diag/right/down and p (with
-//             a one-pixel halo) in shared memory for the whole solve. Only
-//             tile-boundary z and p leave the SM, as LL words (see below);
-//             2 grid all-reduces per iteration (p.q; r.r and r.z).
-//   streaming (large rasters): sweep A recomputes p = r/diag + beta p_prev
-//             at the 4 neighbours (no halo exchange), q = H p, p.q; sweep B
-//             x += a p, r -= a q, r.r, r.z; both stream from L2/HBM.
-//
-// Grid all-reduce = the LL protocol (as in NCCL's LL): each CTA publishes its
-// partial sums as 64-bit words {32-bit half of a double, 32-bit flag};
-// 64-bit stores are single-copy atomic, so a reader that sees the flag sees
-// the data. Every CTA polls every other CTA's words (loads of all slots in
-// flight at once), then sums them in a fixed order. Measured on B200 at 148
-// CTAs: 1.9 us per all-reduce vs 4.1 us for tag+acquire slots and 2.8 us for
-// an atomic arrival counter (scripts/sync_bench.py, profiles/). A trailing
-// fence is added when the reduction must also publish other global writes.
+// fusion.cu -- host side of the fusion optimiser and its small kernels
+// (k_fusion_banded, k_gradient, k_stencil_apply, k_sync_bench). The device
+// code and the design notes are in fusion_impl.cuh; the k_fusion<PPT, VAR>
+// instantiations live in fusion_part_*.cu.
 #include <math.h>
 #include <stdio.h>
 
@@ -44,1209 +9,9 @@
 #include <climits>
 #include <vector>
 
-#include "common.cuh"
-#include "fusion.cuh"
+#include "fusion_impl.cuh"
 
 namespace dfuse_cuda {
-#ifndef DFUSE_FT
-#define DFUSE_FT 512
-#endif
-
-constexpr int FT = DFUSE_FT;  // threads per CTA (one CTA per SM)
-constexpr int FW = FT / 32;
-
-struct Sel {
-  bool net, grad, scale;
-};
-
-__device__ __forceinline__ Sel terms_for(int mode) {  // fusion.hpp:151-158
-  Sel s{true, true, true};
-  if (mode == DFUSE_MODE_NOPAIRWISE) s.grad = false;
-  if (mode == DFUSE_MODE_LSSCALE) {
-    s.net = false;
-    s.scale = false;
-  }
-  return s;
-}
-
-__device__ __forceinline__ double huber_w(double r, double delta) {  // fusion.hpp:79-83
-  const double a = fabs(r);
-  return a <= delta ? 1.0 : delta / a;
-}
-__device__ __forceinline__ double huber_c(double r, double delta) {  // fusion.hpp:87-90
-  const double a = fabs(r);
-  return a <= delta ? r * r : delta * (2.0 * a - delta);
-}
-__device__ __forceinline__ double semi_logvar(double v, double d) {  // fusion.hpp:98-100
-  const double x = v / (d * d);
-  return x < 1e-4 ? 1e-4 : x;
-}
-
-// ---------------------------------------------------------------------------
-// memory-model helpers
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// LL words: word 0 = low half, word 1 = high half of the double
-__device__ __forceinline__ unsigned long long ll_word(double v, int half, unsigned flag) {
-  const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
-  const unsigned h = half ? (unsigned)(bits >> 32) : (unsigned)bits;
-  return ((unsigned long long)flag << 32) | h;
-}
-__device__ __forceinline__ double ll_value(unsigned long long w0, unsigned long long w1) {
-  return __longlong_as_double(
-      (long long)(((w1 & 0xffffffffULL) << 32) | (w0 & 0xffffffffULL)));
-}
-// the two words of one double travel in one 16-byte access (each 8-byte
-// element is single-copy atomic, which is all the LL protocol needs)
-__device__ __forceinline__ void ld_relaxed_v2(const unsigned long long* p, unsigned long long& a,
-                                              unsigned long long& b) {
-  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
-               : "=l"(a), "=l"(b)
-               : "l"(p)
-               : "memory");
-}
-__device__ __forceinline__ void st_relaxed_v2(unsigned long long* p, unsigned long long a,
-                                              unsigned long long b) {
-  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b)
-               : "memory");
-}
-__device__ __forceinline__ void ll_store(unsigned long long* p, double v, unsigned flag) {
-#if DFUSE_LL_V2_HALO
-  st_relaxed_v2(p, ll_word(v, 0, flag), ll_word(v, 1, flag));
-#else
-  st_relaxed_u64(p, ll_word(v, 0, flag));
-  st_relaxed_u64(p + 1, ll_word(v, 1, flag));
-#endif
-}
-__device__ __forceinline__ double ll_wait(const unsigned long long* p, unsigned flag) {
-  unsigned long long w0, w1;
-  do {
-    ld_relaxed_v2(p, w0, w1);
-  } while ((unsigned)(w0 >> 32) != flag || (unsigned)(w1 >> 32) != flag);
-  return ll_value(w0, w1);
-}
-
-// ---------------------------------------------------------------------------
-// grid all-reduce
-struct GridCtx {
-  static constexpr bool kHier = false;
-  ReduceSlot* slots;  // LL slot array (fusion_slots_bytes)
-  unsigned G;
-  unsigned long long base_tag;  // atomic-counter microbenchmark variant only
-  unsigned phase;
-  int syncs;
-  unsigned ll_next;  // next free LL flag for the resident PCG halo exchange
-};
-
-// Row-band launch: the CTAs of band b form one LL all-reduce
-// group (slots = the band's level-1 array, G = CTAs per band, me = index in
-// the band); the band totals then travel through level-2 LL arrays, one per
-// band, into which every band's leader CTA posts its total (remote stores
-// when bands sit on different GPUs) and which the band's own CTAs poll; each
-// CTA adds the band totals in band order, so every CTA of every band holds
-// the same bits.
-struct BandCtx : GridCtx {
-  static constexpr bool kHier = true;
-  unsigned me, band, nband;
-  unsigned long long* const* rank_slots;  // [nband] level-2 arrays
-  int sys;  // fences at system scope (bands on several GPUs)
-};
-
-template <class Ctx>
-__device__ __forceinline__ unsigned cta_index(const Ctx& c) {
-  if constexpr (Ctx::kHier)
-    return c.me;
-  else
-    return blockIdx.x;
-}
-template <class Ctx>
-__device__ __forceinline__ void ctx_fence(const Ctx& c) {
-  if constexpr (Ctx::kHier) {
-    if (c.sys) {
-      __threadfence_system();
-      return;
-    }
-  }
-  __threadfence();
-}
-
-// LL all-reduce slots: value k of CTA b in phase parity q is one 16-byte
-// {low, high} LL pair at its own 256-byte stride (the L2 hashes 256-byte
-// granules over its slices; every CTA polls every slot).
-constexpr int kSlotWords = 32;  // 256 bytes
-__device__ __forceinline__ unsigned long long* ll_slot(const GridCtx& c, unsigned phase, int k,
-                                                       unsigned b) {
-  return reinterpret_cast<unsigned long long*>(c.slots) +
-         (((size_t)(phase & 1) * 4 + k) * c.G + b) * kSlotWords;
-}
-
-// CTA-local first stage: every thread's v summed in a fixed order; the
-// result is valid in warp 0 (returned in t)
-template <int NV>
-__device__ __forceinline__ void cta_partial(double (&v)[NV], double (&t)[NV], double* red) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < NV; ++k) red[wid * 4 + k] = v[k];
-  __syncthreads();
-  if (wid == 0)
-#pragma unroll
-    for (int k = 0; k < NV; ++k) t[k] = warp_sum(lane < FW ? red[lane * 4 + k] : 0.0);
-}
-
-// warp 0 posts the CTA's partials: lane k stores value k as one LL pair
-template <int NV, class Ctx>
-__device__ __forceinline__ void ll_publish(const Ctx& c, const double (&t)[NV]) {
-  const int lane = threadIdx.x & 31;
-  if (lane < NV) {
-    double tk = t[0];
-#pragma unroll
-    for (int k = 1; k < NV; ++k)
-      if (lane == k) tk = t[k];
-    st_relaxed_v2(ll_slot(c, c.phase, lane, cta_index(c)), ll_word(tk, 0, c.phase + 1),
-                  ll_word(tk, 1, c.phase + 1));
-  }
-}
-
-// Warps 0..kPollWarps-1 poll the slots: lane l of warp w owns slot
-// b = l + 32 (w + kPollWarps m). Each round loads all of the lane's slots at
-// once and sums them speculatively; the round whose flags all match wins.
-// A round's latency grows with the loads per lane, so the slots are spread
-// over several warps (one slot per lane at G <= 32 kPollWarps). Measured at
-// G = 148: one polling warp (5 slots per lane) 3.7 us per PCG all-reduce,
-// five warps 1.7 us; all 16 warps with one (slot, value) pair per lane is
-// slower again (the final barrier waits on more warps). Per-warp sums land in
-// pol[w][k]; poll_total adds them in warp order (same bits in every CTA).
-constexpr int kPollWarps = 5;
-constexpr int kMaxPollSlots = 2;  // slots per lane: grids up to 32*5*2 = 320 CTAs
-template <int NV, bool FENCE, class Ctx>
-__device__ __forceinline__ void ll_poll(const Ctx& c, double* pol, long long* rec) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (wid >= kPollWarps) return;
-  const unsigned flag = c.phase + 1;
-  double acc[NV];
-  for (;;) {
-    bool ok = true;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) acc[k] = 0.0;
-#pragma unroll
-    for (int m = 0; m < kMaxPollSlots; ++m) {
-      const unsigned b = lane + 32 * (wid + kPollWarps * m);
-      if (b < c.G) {
-#pragma unroll
-        for (int k = 0; k < NV; ++k) {
-          unsigned long long w0, w1;
-          ld_relaxed_v2(ll_slot(c, c.phase, k, b), w0, w1);
-          ok &= (unsigned)(w0 >> 32) == flag && (unsigned)(w1 >> 32) == flag;
-          acc[k] += ll_value(w0, w1);
-        }
-      }
-    }
-    if (rec && threadIdx.x == 0) rec[3] += 1;  // diagnostics: poll rounds of warp 0
-    if (__all_sync(0xffffffffu, ok)) break;
-  }
-  if (FENCE) ctx_fence(c);
-#pragma unroll
-  for (int k = 0; k < NV; ++k) acc[k] = warp_sum(acc[k]);
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < NV; ++k) pol[wid * 4 + k] = acc[k];
-}
-
-template <int NV>
-__device__ __forceinline__ void poll_total(const double* pol, double (&v)[NV]) {
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    double s = pol[k];
-#pragma unroll
-    for (int w = 1; w < kPollWarps; ++w) s += pol[w * 4 + k];
-    v[k] = s;
-  }
-}
-
-// Sum v[0..NV) (NV <= 4) over every thread of the grid; identical bits in
-// every thread (every CTA adds the same partials in the same order).
-// FENCE: also order every global write made before the call before every
-// global read after it, grid-wide (needed whenever other CTAs read data this
-// CTA wrote). VARIANT 10 = LL all-to-all (production); 2 = atomic arrival
-// counter (sync microbenchmark baseline). rec: DFUSE_TRACE=3 timestamps.
-// level 2 of a banded all-reduce: v (the band total, identical in every CTA
-// of the band) -> the sum of all band totals in band order
-template <int NV, bool FENCE>
-__device__ void band_exchange(BandCtx& c, double (&v)[NV]) {
-  __shared__ double pol2[4];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (wid == 0) {
-    const unsigned flag = c.phase + 1;
-    auto slot = [&](unsigned h, int k, unsigned src) {
-      return c.rank_slots[h] + (((size_t)(c.phase & 1) * 4 + k) * c.nband + src) * kSlotWords;
-    };
-    if (lane < NV) {
-      double tk = v[0];
-#pragma unroll
-      for (int k = 1; k < NV; ++k)
-        if (lane == k) tk = v[k];
-      if (c.me == 0)  // the band's leader posts the band total to every band
-        for (unsigned h = 0; h < c.nband; ++h)
-          st_relaxed_v2(slot(h, lane, c.band), ll_word(tk, 0, flag), ll_word(tk, 1, flag));
-      double sum;
-      for (;;) {
-        bool ok = true;
-        sum = 0.0;
-        for (unsigned h = 0; h < c.nband; ++h) {
-          unsigned long long w0, w1;
-          ld_relaxed_v2(slot(c.band, lane, h), w0, w1);
-          ok &= (unsigned)(w0 >> 32) == flag && (unsigned)(w1 >> 32) == flag;
-          sum += ll_value(w0, w1);
-        }
-        if (ok) break;
-      }
-      pol2[lane] = sum;
-    }
-    if (FENCE) ctx_fence(c);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < NV; ++k) v[k] = pol2[k];
-}
-
-template <int NV, bool FENCE = true, int VARIANT = 10, class Ctx = GridCtx>
-__device__ void grid_allreduce(Ctx& c, double (&v)[NV], long long* rec = nullptr) {
-  __shared__ double red[FW * 4];
-  __shared__ double pol[kPollWarps * 4];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (rec && threadIdx.x == 0) rec[0] = clock64();
-  double t[NV];
-  cta_partial(v, t, red);
-  if (VARIANT == 10) {
-    if (wid == 0) {
-      // release: the CTA's earlier global writes (ordered before this point
-      // by the barrier in cta_partial) become visible before the LL words
-      if (FENCE) ctx_fence(c);
-      if (rec && lane == 0) rec[1] = clock64();
-      ll_publish(c, t);
-    }
-    ll_poll<NV, FENCE>(c, pol, rec);
-    if (rec && threadIdx.x == 0) rec[2] = clock64();
-    __syncthreads();
-    poll_total(pol, v);
-    if constexpr (Ctx::kHier) {
-      if (c.nband > 1) band_exchange<NV, FENCE>(c, v);
-    }
-  } else {
-    ReduceSlot* buf = c.slots + (size_t)(c.phase & 1) * c.G;
-    if (wid == 0) {
-      if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < NV; ++k) buf[blockIdx.x].v[k] = t[k];
-        __threadfence();
-        atomicAdd(reinterpret_cast<unsigned*>(c.slots + 2 * c.G), 1u);
-        const unsigned target = (c.phase + 1) * c.G;
-        while (ld_acquire(reinterpret_cast<unsigned*>(c.slots + 2 * c.G)) < target) {
-        }
-      }
-      __syncwarp();
-      __threadfence();
-      double acc[NV];
-#pragma unroll
-      for (int k = 0; k < NV; ++k) acc[k] = 0.0;
-      for (unsigned b = lane; b < c.G; b += 32)
-#pragma unroll
-        for (int k = 0; k < NV; ++k) acc[k] += __ldcg(&buf[b].v[k]);
-#pragma unroll
-      for (int k = 0; k < NV; ++k) acc[k] = warp_sum(acc[k]);
-      if (lane == 0)
-#pragma unroll
-        for (int k = 0; k < NV; ++k) pol[k] = acc[k];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < NV; ++k) v[k] = pol[k];
-  }
-  if (rec && threadIdx.x == 0) rec[4] = clock64();
-  c.phase += 1;
-  c.syncs += 1;
-}
-
-template <class Ctx>
-__device__ __forceinline__ void grid_sync(Ctx& c) {
-  double none[1] = {0.0};
-  grid_allreduce(c, none);
-}
-
-// Split-phase LL all-reduce (no fence): publish() reduces the CTA's partials
-// and posts them; the CTA may then do independent work (the resident PCG
-// runs its next SpMV there) before wait() collects the grid sum. No other
-// all-reduce may run in between.
-__device__ __forceinline__ double* split_smem() {
-  __shared__ double s[FW * 4 + kPollWarps * 4];
-  return s;
-}
-
-template <int NV>
-__device__ void grid_allreduce_publish(GridCtx& c, double (&v)[NV]) {
-  double t[NV];
-  cta_partial(v, t, split_smem());
-  if ((threadIdx.x >> 5) == 0) ll_publish(c, t);
-}
-
-template <int NV>
-__device__ void grid_allreduce_wait(GridCtx& c, double (&v)[NV]) {
-  double* pol = split_smem() + FW * 4;
-  ll_poll<NV, false>(c, pol, nullptr);
-  __syncthreads();
-  poll_total(pol, v);
-  c.phase += 1;
-  c.syncs += 1;
-}
-
-// ---------------------------------------------------------------------------
-// per-pixel terms (gather form)
-struct PlainLd {
-  static constexpr bool kTrial = false;
-  const double* ld;
-  __device__ __forceinline__ double operator()(int j) const { return ld[j]; }
-};
-struct TrialLd {  // trial.log_depth = st + step * delta, fusion.hpp:432-433
-  static constexpr bool kTrial = true;
-  const double* ld;
-  const double* x;
-  double step;
-  __device__ __forceinline__ double operator()(int j) const { return ld[j] + step * x[j]; }
-};
-
-// total_cost's contribution of pixel i with the reference's own arithmetic
-// (fusion.hpp:234-250; divisions by the variances). Used by k_gradient, the
-// test-only cost_gradient kernel.
-template <class LD>
-__device__ __forceinline__ double pixel_cost_exact(const FusionArgs& a, const Sel& sel, int i,
-                                                   int x, int y, const LD& L, double li,
-                                                   double ln_s) {
-  double c = 0.0;
-  if (sel.net) c += huber_c(li - a.pred[0][i], a.dnet) / a.pred[1][i];
-  if (a.svalid[i])
-    c += huber_c(li - ln_s - log(a.sd[i]), a.dsemi) / semi_logvar(a.sv[i], a.sd[i]);
-  if (sel.grad && x + 1 < a.W) c += huber_c(L(i + 1) - li - a.pred[2][i], a.dgrad) / a.pred[3][i];
-  if (sel.grad && y + 1 < a.H)
-    c += huber_c(L(i + a.W) - li - a.pred[4][i], a.dgrad) / a.pred[5][i];
-  return c;
-}
-
-struct Range {
-  int beg, end;
-};
-
-__device__ __forceinline__ Range my_range(const FusionArgs& a) {
-  Range r;
-  if (a.band_ctas > 0) {  // the band's rows among the band's CTAs
-    const long b0 = (long)a.band_y0 * a.W, len = (long)(a.band_y1 - a.band_y0) * a.W;
-    const long k = (long)blockIdx.x - a.band_cta0;
-    r.beg = (int)(b0 + len * k / a.band_ctas);
-    r.end = (int)(b0 + len * (k + 1) / a.band_ctas);
-  } else {
-    const long P = (long)a.W * a.H;
-    r.beg = (int)(P * blockIdx.x / gridDim.x);
-    r.end = (int)(P * (blockIdx.x + 1) / gridDim.x);
-  }
-  return r;
-}
-
-// the neighbour band's copy of a boundary-row value (no-op unless banded)
-__device__ __forceinline__ void halo_put(const BandNb* nb, int y0, int y1, int plane, int i, int y,
-                                         double v) {
-  if (nb) {
-    if (y == y0 && nb->up[plane]) nb->up[plane][i] = v;
-    if (y == y1 - 1 && nb->dn[plane]) nb->dn[plane][i] = v;
-  }
-}
-__device__ __forceinline__ void halo_put(const FusionArgs& a, int plane, int i, double v) {
-  if (a.nb) halo_put(a.nb, a.band_y0, a.band_y1, plane, i, i / a.W, v);
-}
-
-// ---------------------------------------------------------------------------
-// sweeps (every sweep walks the CTA's range with the same thread->pixel map,
-// so per-pixel values a thread writes are read back by that thread).
-//
-// The sweeps are latency-bound gathers from L2, so they are written for
-// memory-level parallelism: each thread walks its pixels in fully unrolled,
-// predicated groups of U; every load of a pixel is unconditional (indices
-// clamped to the pixel itself where the reference skips a term) and the
-// skipped terms are removed with selects, and the arrays come in as
-// __restrict__ parameters, so the compiler can issue all of a group's loads
-// before the first result is needed (a branch per term, or a possibly
-// aliasing store, would serialise one L2 round trip per term).
-//
-// Per-call planes (sweep_prologue): ln d_semi and 1/R_semi (0 where the semi
-// map has no value) and the reciprocals of the three prediction variances.
-// Each weighted term is then huber * (1/var) where the reference computes
-// huber / var: equal up to one rounding (tolerance parity).
-
-struct SweepPlanes {
-  const double* __restrict__ p0;  // pred log_depth
-  const double* __restrict__ p2;  // pred grad_x
-  const double* __restrict__ p4;  // pred grad_y
-  const double* __restrict__ iv0;  // 1 / log_depth_var
-  const double* __restrict__ iv1;  // 1 / grad_x_var
-  const double* __restrict__ iv2;  // 1 / grad_y_var
-  const uint8_t* __restrict__ sval;
-  const double* __restrict__ lns;  // ln d_semi (0 if invalid)
-  const double* __restrict__ irs;  // 1 / semi_log_variance (0 if invalid)
-};
-
-__device__ __forceinline__ SweepPlanes planes_of(const FusionArgs& a) {
-  return SweepPlanes{a.pred[0], a.pred[2], a.pred[4], a.ivar[0], a.ivar[1],
-                     a.ivar[2], a.svalid, a.lnsd, a.irs};
-}
-
-__device__ void sweep_prologue(const FusionArgs& a, const Range& rg) {
-  for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) {
-    const bool v = a.svalid[i];
-    const double d = a.sd[i];
-    a.lnsd[i] = v ? log(d) : 0.0;                          // fusion.hpp:195
-    a.irs[i] = v ? 1.0 / semi_logvar(a.sv[i], d) : 0.0;    // fusion.hpp:95-100,196
-    a.ivar[0][i] = 1.0 / a.pred[1][i];
-    a.ivar[1][i] = 1.0 / a.pred[3][i];
-    a.ivar[2][i] = 1.0 / a.pred[5][i];
-    halo_put(a, HP_IV2, i, a.ivar[2][i]);
-  }
-}
-
-// one pixel's total_cost terms (fusion.hpp:234-250, reference order) from
-// loaded values; lr / ldn = log-depth at i+1 / i+W (any value when absent)
-__device__ __forceinline__ double cost_terms(const Sel sel, const bool hasr, const bool hasd,
-                                             const double li, const double lr, const double ldn,
-                                             const double q0, const double i0, const bool sv,
-                                             const double ln, const double ir, const double q2,
-                                             const double i1, const double q4, const double i2,
-                                             const double dnet, const double dsemi,
-                                             const double dgrad, const double ln_s) {
-  double c = 0.0;
-  if (sel.net) c += huber_c(li - q0, dnet) * i0;
-  const double ts = huber_c(li - ln_s - ln, dsemi) * ir;
-  c += sv ? ts : 0.0;
-  if (sel.grad) {
-    const double tx = huber_c(lr - li - q2, dgrad) * i1;
-    c += hasr ? tx : 0.0;
-    const double ty = huber_c(ldn - li - q4, dgrad) * i2;
-    c += hasd ? ty : 0.0;
-  }
-  return c;
-}
-
-// total_cost of ld (+ step * xs when TRIAL); wt: also store the evaluated
-// log-depth (the trial state)
-template <int U, bool TRIAL>
-__device__ __forceinline__ double sweep_cost_body(const Range rg, const int W, const int H,
-                                                  const Sel sel, const double dnet,
-                                                  const double dsemi, const double dgrad,
-                                                  const double ln_s, const double* __restrict__ ld,
-                                                  const double* __restrict__ xs, const double step,
-                                                  const SweepPlanes pl, double* __restrict__ wt,
-                                                  const BandNb* nb, const int y0, const int y1,
-                                                  const int wt_plane) {
-  double cost = 0.0;
-  for (int i0 = rg.beg + threadIdx.x; i0 < rg.end; i0 += U * FT) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int iu = i0 + u * FT;
-      const bool in = iu < rg.end;
-      const int i = in ? iu : rg.beg;
-      const int y = i / W, x = i - y * W;
-      const bool hasr = x + 1 < W, hasd = y + 1 < H;
-      const int ir = hasr ? i + 1 : i, id = hasd ? i + W : i;
-      const double li = TRIAL ? ld[i] + step * xs[i] : ld[i];
-      const double lr = TRIAL ? ld[ir] + step * xs[ir] : ld[ir];
-      const double ldn = TRIAL ? ld[id] + step * xs[id] : ld[id];
-      const double c = cost_terms(sel, hasr, hasd, li, lr, ldn, pl.p0[i], pl.iv0[i], pl.sval[i],
-                                  pl.lns[i], pl.irs[i], pl.p2[i], pl.iv1[i], pl.p4[i], pl.iv2[i],
-                                  dnet, dsemi, dgrad, ln_s);
-      if (in) {
-        if (wt) {
-          wt[i] = li;
-          halo_put(nb, y0, y1, wt_plane, i, y, li);
-        }
-        cost += c;
-      }
-    }
-  }
-  return cost;
-}
-
-template <int U, class LD>
-__device__ double sweep_cost(const FusionArgs& a, const Sel& sel, const Range& rg, const LD& L,
-                             double ln_s, double* write_trial) {
-  const int wplane = write_trial == a.ld[0] ? HP_LD0 : HP_LD1;
-  if constexpr (LD::kTrial)  // trial = st + step * delta (fusion.hpp:432-433)
-    return sweep_cost_body<U, true>(rg, a.W, a.H, sel, a.dnet, a.dsemi, a.dgrad, ln_s, L.ld, L.x,
-                                    L.step, planes_of(a), write_trial, a.nb, a.band_y0,
-                                    a.band_y1, wplane);
-  else
-    return sweep_cost_body<U, false>(rg, a.W, a.H, sel, a.dnet, a.dsemi, a.dgrad, ln_s, L.ld,
-                                     nullptr, 0.0, planes_of(a), write_trial, a.nb, a.band_y0,
-                                     a.band_y1, wplane);
-}
-
-// scale IRLS round (fusion.hpp:379-388) [+ total_cost at ln_s_cost]
-// stage (optional, shared memory): offset and 1/R of the CTA's pixels for the
-// later rounds (1/R = -1 marks a pixel without a semi-dense value)
-template <int U>
-__device__ __forceinline__ void sweep_scale_body(const Range rg, const int W, const int H,
-                                                 const Sel sel, const double dnet,
-                                                 const double dsemi, const double dgrad,
-                                                 const double* __restrict__ ld, const double ln_s,
-                                                 const bool with_cost, const double ln_s_cost,
-                                                 const SweepPlanes pl, double (&v)[4],
-                                                 double* __restrict__ stage, const int stage_n) {
-  double num = 0.0, den = 0.0, cost = 0.0;
-  for (int i0 = rg.beg + threadIdx.x; i0 < rg.end; i0 += U * FT) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int iu = i0 + u * FT;
-      const bool in = iu < rg.end;
-      const int i = in ? iu : rg.beg;
-      const double li = ld[i];
-      const bool sv = pl.sval[i];
-      const double ln = pl.lns[i], ir = pl.irs[i];
-      const double offset = li - ln;
-      const double wi = huber_w(offset - ln_s, dsemi) * ir;
-      if (in) {
-        num += sv ? wi * offset : 0.0;
-        den += sv ? wi : 0.0;
-        if (stage) {
-          stage[i - rg.beg] = offset;
-          stage[stage_n + i - rg.beg] = sv ? ir : -1.0;
-        }
-      }
-      if (with_cost) {
-        const int y = i / W, x = i - y * W;
-        const bool hasr = x + 1 < W, hasd = y + 1 < H;
-        const double c = cost_terms(sel, hasr, hasd, li, ld[hasr ? i + 1 : i],
-                                    ld[hasd ? i + W : i], pl.p0[i], pl.iv0[i], sv, ln, ir,
-                                    pl.p2[i], pl.iv1[i], pl.p4[i], pl.iv2[i], dnet, dsemi, dgrad,
-                                    ln_s_cost);
-        if (in) cost += c;
-      }
-    }
-  }
-  v[0] = num;
-  v[1] = den;
-  v[2] = cost;
-  v[3] = 0.0;
-}
-
-template <int U>
-__device__ void sweep_scale(const FusionArgs& a, const Sel& sel, const Range& rg,
-                            const double* ld, double ln_s, bool with_cost, double ln_s_cost,
-                            double (&v)[4], double* stage = nullptr, int stage_n = 0) {
-  sweep_scale_body<U>(rg, a.W, a.H, sel, a.dnet, a.dsemi, a.dgrad, ld, ln_s, with_cost, ln_s_cost,
-                      planes_of(a), v, stage, stage_n);
-}
-
-// scale IRLS rounds 1 and 2 from the values staged by round 0 (same
-// arithmetic, same per-thread order as sweep_scale)
-__device__ void sweep_scale_staged(const FusionArgs& a, const Range& rg, const double* stage,
-                                   int stage_n, double ln_s, double (&v)[2]) {
-  double num = 0.0, den = 0.0;
-  for (int k = threadIdx.x; k < rg.end - rg.beg; k += FT) {
-    const double ir = stage[stage_n + k];
-    const double offset = stage[k];
-    const double wi = huber_w(offset - ln_s, a.dsemi) * ir;
-    const bool sv = ir != -1.0;
-    num += sv ? wi * offset : 0.0;
-    den += sv ? wi : 0.0;
-  }
-  v[0] = num;
-  v[1] = den;
-}
-
-// assemble_normal_equations in gather form (fusion.hpp:183-219). For pixel
-// i the reference's scatter loop adds, in raster order of the contributing
-// pixel: grad_y of i-W, grad_x of i-1, then net, semi, grad_x, grad_y of i.
-// Also: PCG init (r = b, z = r/diag, r.z, b.b, diag > 0 check,
-// fusion.hpp:319-332) and the depth block's c0 (fusion.hpp:429).
-template <int U>
-__device__ __forceinline__ void sweep_assemble_body(
-    const Range rg, const int W, const int H, const Sel sel, const double dnet, const double dsemi,
-    const double dgrad, const double* __restrict__ ld, const double ln_s, const SweepPlanes pl,
-    double* __restrict__ o_diag, double* __restrict__ o_right, double* __restrict__ o_down,
-    double* __restrict__ o_r, double* __restrict__ o_b, double* __restrict__ o_z, double (&v)[4],
-    const BandNb* nb, const int y0, const int y1) {
-  double bn = 0.0, rz = 0.0, bad = 0.0, cost = 0.0;
-  for (int i0 = rg.beg + threadIdx.x; i0 < rg.end; i0 += U * FT) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int iu = i0 + u * FT;
-      const bool in = iu < rg.end;
-      const int i = in ? iu : rg.beg;
-      const int y = i / W, x = i - y * W;
-      const bool hasu = sel.grad && y > 0, hasl = sel.grad && x > 0;
-      const bool hasr = x + 1 < W, hasd = y + 1 < H;
-      const int ju = hasu ? i - W : i, jl = hasl ? i - 1 : i;
-      const int jr = hasr ? i + 1 : i, jd = hasd ? i + W : i;
-      const double li = ld[i], lu = ld[ju], ll = ld[jl], lr = ld[jr], ldn = ld[jd];
-      const double q0 = pl.p0[i], i0v = pl.iv0[i], q2 = pl.p2[i], i1 = pl.iv1[i];
-      const double q4 = pl.p4[i], i2 = pl.iv2[i];
-      const bool sv = pl.sval[i];
-      const double ln = pl.lns[i], ir = pl.irs[i];
-      const double q4u = pl.p4[ju], i2u = pl.iv2[ju], q2l = pl.p2[jl], i1l = pl.iv1[jl];
-      double diag = 0.0, b = 0.0, right = 0.0, down = 0.0;
-      {  // grad_y of i-W
-        const double r = li - lu - q4u;
-        const double wi = huber_w(r, dgrad) * i2u;
-        diag += hasu ? wi : 0.0;
-        b -= hasu ? wi * r : 0.0;
-      }
-      {  // grad_x of i-1
-        const double r = li - ll - q2l;
-        const double wi = huber_w(r, dgrad) * i1l;
-        diag += hasl ? wi : 0.0;
-        b -= hasl ? wi * r : 0.0;
-      }
-      if (sel.net) {
-        const double r = li - q0;
-        const double wi = huber_w(r, dnet) * i0v;
-        diag += wi;
-        b -= wi * r;
-      }
-      {  // semi
-        const double r = li - ln_s - ln;
-        const double wi = huber_w(r, dsemi) * ir;
-        diag += sv ? wi : 0.0;
-        b -= sv ? wi * r : 0.0;
-      }
-      const bool gx = sel.grad && hasr, gy = sel.grad && hasd;
-      {  // grad_x of i
-        const double r = lr - li - q2;
-        const double wi = huber_w(r, dgrad) * i1;
-        diag += gx ? wi : 0.0;
-        right -= gx ? wi : 0.0;
-        b += gx ? wi * r : 0.0;
-      }
-      {  // grad_y of i
-        const double r = ldn - li - q4;
-        const double wi = huber_w(r, dgrad) * i2;
-        diag += gy ? wi : 0.0;
-        down -= gy ? wi : 0.0;
-        b += gy ? wi * r : 0.0;
-      }
-      const double c = cost_terms(sel, hasr, hasd, li, lr, ldn, q0, i0v, sv, ln, ir, q2, i1, q4,
-                                  i2, dnet, dsemi, dgrad, ln_s);
-      if (in) {
-        o_diag[i] = diag;
-        o_right[i] = right;
-        o_down[i] = down;
-        o_r[i] = b;
-        halo_put(nb, y0, y1, HP_DOWN, i, y, down);
-        if (o_b) o_b[i] = b;
-        const double z = b / diag;  // PCG init z = r/diag, fusion.hpp:329
-        if (o_z) {
-          o_z[i] = z;
-          halo_put(nb, y0, y1, HP_Z, i, y, z);
-        }
-        bn += b * b;
-        if (!(diag > 0.0)) bad += 1.0;
-        rz += b * z;
-        cost += c;
-      }
-    }
-  }
-  v[0] = bn;
-  v[1] = rz;
-  v[2] = bad;
-  v[3] = cost;
-}
-
-template <int U>
-__device__ void sweep_assemble(const FusionArgs& a, const Sel& sel, const Range& rg,
-                               const double* ld, double ln_s, bool store_b, double (&v)[4]) {
-  sweep_assemble_body<U>(rg, a.W, a.H, sel, a.dnet, a.dsemi, a.dgrad, ld, ln_s, planes_of(a),
-                         a.diag, a.right, a.down, a.r, store_b ? a.b : nullptr, a.z, v, a.nb,
-                         a.band_y0, a.band_y1);
-}
-
-// standalone PCG init from (diag, right, down, b)
-__device__ void sweep_pcg_init(const FusionArgs& a, const Range& rg, double (&v)[4]) {
-  double bn = 0.0, rz = 0.0, bad = 0.0;
-  for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) {
-    const double b = a.b[i], d = a.diag[i];
-    a.r[i] = b;
-    const double z = b / d;  // fusion.hpp:329
-    if (a.z) a.z[i] = z;
-    bn += b * b;
-    if (!(d > 0.0)) bad += 1.0;
-    rz += b * z;
-  }
-  v[0] = bn;
-  v[1] = rz;
-  v[2] = bad;
-  v[3] = 0.0;
-}
-
-__device__ void sweep_zero_x(const FusionArgs& a, const Range& rg) {
-  for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) {
-    a.x[i] = 0.0;
-    halo_put(a, HP_X, i, 0.0);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// streaming PCG (rasters too large for the SM-resident tiles, e.g. C4's 4K).
-// z = r/diag is stored by the sweep that updates r (one IEEE division per
-// pixel, fusion.hpp:329,359), so sweep A rebuilds p at the four neighbours
-// from (z, p_prev) alone. Both sweeps are written like the Gauss-Newton
-// sweeps: unrolled predicated pixel groups, unconditional clamped loads,
-// skipped stencil terms removed by selects, __restrict__ planes.
-
-// sweep A: p = z + beta p_prev (p = z at it 0, fusion.hpp:329-330,364),
-// q = H p in StencilMatrix::apply order (fusion.hpp:127-132); returns p.q
-template <int U, bool FIRST>
-__device__ __forceinline__ double sweep_pcg_a_body(
-    const Range rg, const int W, const int H, const double beta, const double* __restrict__ z,
-    const double* __restrict__ pprev, const double* __restrict__ diag,
-    const double* __restrict__ right, const double* __restrict__ down, double* __restrict__ pcur,
-    double* __restrict__ q, const BandNb* nb, const int y0, const int y1, const int pplane) {
-  double pq = 0.0;
-  for (int i0 = rg.beg + threadIdx.x; i0 < rg.end; i0 += U * FT) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int iu = i0 + u * FT;
-      const bool in = iu < rg.end;
-      const int i = in ? iu : rg.beg;
-      const int y = i / W, x = i - y * W;
-      const bool hr = x + 1 < W, hl = x > 0, hd = y + 1 < H, hu = y > 0;
-      const int jr = hr ? i + 1 : i, jl = hl ? i - 1 : i, jd = hd ? i + W : i, ju = hu ? i - W : i;
-      const double pc = FIRST ? z[i] : z[i] + beta * pprev[i];
-      const double pr = FIRST ? z[jr] : z[jr] + beta * pprev[jr];
-      const double pl = FIRST ? z[jl] : z[jl] + beta * pprev[jl];
-      const double pd = FIRST ? z[jd] : z[jd] + beta * pprev[jd];
-      const double pu = FIRST ? z[ju] : z[ju] + beta * pprev[ju];
-      const double tr = right[i] * pr, tl = right[jl] * pl, td = down[i] * pd, tu = down[ju] * pu;
-      double v = diag[i] * pc;
-      v += hr ? tr : 0.0;
-      v += hl ? tl : 0.0;
-      v += hd ? td : 0.0;
-      v += hu ? tu : 0.0;
-      if (in) {
-        pcur[i] = pc;
-        halo_put(nb, y0, y1, pplane, i, y, pc);
-        q[i] = v;
-        pq += pc * v;
-      }
-    }
-  }
-  return pq;
-}
-
-template <int U>
-__device__ double sweep_pcg_a(const FusionArgs& a, const Range& rg, int it, double beta) {
-  const int pplane = (it & 1) ? HP_P1 : HP_P0;
-  if (it == 0)
-    return sweep_pcg_a_body<U, true>(rg, a.W, a.H, beta, a.z, a.p[(it + 1) & 1], a.diag, a.right,
-                                     a.down, a.p[it & 1], a.q, a.nb, a.band_y0, a.band_y1, pplane);
-  return sweep_pcg_a_body<U, false>(rg, a.W, a.H, beta, a.z, a.p[(it + 1) & 1], a.diag, a.right,
-                                    a.down, a.p[it & 1], a.q, a.nb, a.band_y0, a.band_y1, pplane);
-}
-
-// sweep B (fusion.hpp:345-362): x += alpha p, r -= alpha q, z = r/diag;
-// returns (r.r, r.z)
-template <int U>
-__device__ __forceinline__ void sweep_pcg_b_body(
-    const Range rg, const int W, const bool first, const double alpha,
-    const double* __restrict__ pcur, const double* __restrict__ q, const double* __restrict__ diag,
-    double* __restrict__ x, double* __restrict__ r, double* __restrict__ z, const BandNb* nb,
-    const int y0, const int y1, double (&v)[2]) {
-  double rr = 0.0, rz = 0.0;
-  for (int i0 = rg.beg + threadIdx.x; i0 < rg.end; i0 += U * FT) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int iu = i0 + u * FT;
-      const bool in = iu < rg.end;
-      const int i = in ? iu : rg.beg;
-      const double xo = first ? 0.0 : x[i];
-      const double xn = xo + alpha * pcur[i];
-      const double rn = r[i] - alpha * q[i];
-      const double zn = rn / diag[i];
-      if (in) {
-        const int y = i / W;
-        x[i] = xn;
-        r[i] = rn;
-        z[i] = zn;
-        halo_put(nb, y0, y1, HP_X, i, y, xn);
-        halo_put(nb, y0, y1, HP_Z, i, y, zn);
-        rr += rn * rn;
-        rz += rn * zn;
-      }
-    }
-  }
-  v[0] = rr;
-  v[1] = rz;
-}
-
-template <int U>
-__device__ void sweep_pcg_b(const FusionArgs& a, const Range& rg, int it, double alpha,
-                            double (&v)[2]) {
-  sweep_pcg_b_body<U>(rg, a.W, it == 0, alpha, a.p[it & 1], a.q, a.diag, a.x, a.r, a.z, a.nb,
-                      a.band_y0, a.band_y1, v);
-}
-
-// Jacobi PCG after init (solve_depth_step, fusion.hpp:334-367). Returns the
-// error code (0 ok); *its = iterations run.
-template <int SU, class Ctx>
-__device__ int pcg_stream(Ctx& c, const FusionArgs& a, const Range& rg, double bnorm2,
-                          double rz, int* its) {
-  const double tol2 = a.cg_tol * a.cg_tol * bnorm2;
-  double prev = bnorm2;
-  int streak = 0;
-  double beta = 0.0;
-  *its = 0;
-  for (int it = 0; it < a.cg_max; ++it) {
-    *its = it + 1;
-    double v1[1] = {sweep_pcg_a<SU>(a, rg, it, beta)};
-    grid_allreduce(c, v1);
-    if (!(v1[0] > 0.0)) return DFUSE_E_CG_DIVERGENCE;
-    const double alpha = rz / v1[0];
-    double v2[2];
-    sweep_pcg_b<SU>(a, rg, it, alpha, v2);
-    grid_allreduce(c, v2);
-    const double rn = v2[0];
-    if (rn <= tol2) return 0;
-    if (rn > prev) {
-      if (++streak >= 10) return DFUSE_E_CG_DIVERGENCE;
-    } else {
-      streak = 0;
-    }
-    prev = rn;
-    beta = v2[1] / rz;
-    rz = v2[1];
-  }
-  return 0;
-}
-
-// ---------------------------------------------------------------------------
-// SM-resident PCG tiling (pcg_tile.cuh): CTA b owns tile b of a
-// tiles_x x tiles_y partition of the raster.
-struct TileGeo {
-  int x0, y0, tw, th;  // tw*th == 0 for CTAs without a tile
-};
-
-__device__ __forceinline__ TileGeo my_tile(const FusionArgs& a) {
-  TileGeo t{0, 0, 0, 0};
-  const int nt = a.tiles_x * a.tiles_y;
-  if ((int)blockIdx.x < nt) {
-    const int bx = blockIdx.x % a.tiles_x, by = blockIdx.x / a.tiles_x;
-    t.x0 = (int)((long)a.W * bx / a.tiles_x);
-    t.y0 = (int)((long)a.H * by / a.tiles_y);
-    t.tw = (int)((long)a.W * (bx + 1) / a.tiles_x) - t.x0;
-    t.th = (int)((long)a.H * (by + 1) / a.tiles_y) - t.y0;
-  }
-  return t;
-}
-
-#include "pcg_tile.cuh"
-
-template <int PPT, int VAR, class Ctx>
-__device__ __forceinline__ int pcg_solve(Ctx& c, const FusionArgs& a, const Range& rg,
-                                         double bnorm2, double rz, int* its) {
-  if constexpr (PPT > 0) {
-    if constexpr (VAR == 1) return pcg_resident<PPT>(c, a, bnorm2, rz, its);
-    if constexpr (VAR == 2) return pcg_resident_2r<PPT>(c, a, bnorm2, rz, its);
-    PcgHandover h;
-    const int st = pcg_resident_pipe<PPT>(c, a, bnorm2, rz, its, &h);
-    return st >= 0 ? st : pcg_resume_cg<PPT>(c, a, bnorm2, h, its);
-  } else {
-    const int st = pcg_stream<4>(c, a, rg, bnorm2, rz, its);
-    if (*its == 0) {
-      sweep_zero_x(a, rg);
-      grid_sync(c);
-    }
-    return st;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// optimize() on the device (fusion.hpp:402-454). Ctx: GridCtx (one grid)
-// or BandCtx (row bands, hierarchical all-reduce); every CTA runs the same
-// control flow on identical all-reduced scalars.
-template <int PPT, int VAR, class Ctx>
-__device__ __forceinline__ void optimize_body(Ctx& c, const FusionArgs& a, const Range& rg,
-                                              const Sel& sel, const bool leader, int& status) {
-  constexpr int SU = PPT > 0 ? PPT : 2;  // pixels per thread per unrolled sweep group
-  FusionControl* ctl = a.ctl;
-  // State that lives across the PCG call sits in shared memory where it can,
-  // so the (inlined) PCG loop keeps the register file: the counters (thread
-  // 0 only) and the input state (re-read at the end).
-  __shared__ int gn_cnt[3];     // cost_evals, pcg_total, gn_done
-  double scale = a.st_in->scale;
-  int cur = a.st_in->cur;
-  const int inliers = a.inlier_dev ? *a.inlier_dev : a.inlier_count;
-  const bool ls_mode = a.mode == DFUSE_MODE_LSSCALE;
-  const bool depth_solvable = !ls_mode || inliers > 0;
-  if (threadIdx.x == 0) gn_cnt[0] = gn_cnt[1] = gn_cnt[2] = 0;
-  const bool otr = a.trace && leader;  // DFUSE_TRACE: ns per GN phase, CTA 0
-  __shared__ long long ot[8];          // [7] = last timestamp (thread 0 only)
-  if (otr)
-    for (int k = 0; k < 8; ++k) ot[k] = 0;
-#define DF_OTRACE(k)                \
-if (otr) {                        \
-  const long long t_ = df_now(); \
-  ot[k] += t_ - ot[7];            \
-  ot[7] = t_;                     \
-}
-  const bool scale_block = !ls_mode && a.est_scale && inliers > 0;  // fusion.hpp:411
-  extern __shared__ double dsm_stage[];
-  double* stage = a.stage_n > 0 ? dsm_stage : nullptr;
-  for (int it = 0; it < a.gn && status == 0; ++it) {
-    if (otr) ot[7] = df_now();
-    bool have_eq = false;  // the scale block left an assembly valid for the depth block
-    double veq[4] = {0.0, 0.0, 0.0, 0.0};
-    if (scale_block) {  // fusion.hpp:411-425
-      const double ln_s0 = log(scale);
-      double ln_s = ln_s0;
-      double c0 = 0.0;
-      // the scale sweeps write no global memory, so their all-reduces need
-      // no fence
-      for (int round = 0; round < 3; ++round) {
-        if (round == 0) {
-          double v[4];
-          sweep_scale<SU>(a, sel, rg, a.ld[cur], ln_s, true, sel.scale ? ln_s0 : 0.0, v, stage,
-                          a.stage_n);
-          double w[3] = {v[0], v[1], v[2]};
-          grid_allreduce<3, false>(c, w);
-          c0 = w[2];
-          ln_s = w[0] / w[1];
-        } else {
-          double w[2];
-          if (stage) {
-            sweep_scale_staged(a, rg, stage, a.stage_n, ln_s, w);
-          } else {
-            double v[4];
-            sweep_scale<SU>(a, sel, rg, a.ld[cur], ln_s, false, 0.0, v);
-            w[0] = v[0];
-            w[1] = v[1];
-          }
-          grid_allreduce<2, false>(c, w);
-          ln_s = w[0] / w[1];
-        }
-      }
-      if (threadIdx.x == 0) gn_cnt[0] += 1;
-      DF_OTRACE(0);
-      const double s_new = exp(ln_s);
-      const double dlns = log(s_new) - log(scale);
-      double step = 1.0, accepted = 0.0;
-      for (int half = 0; half <= 5; ++half) {
-        const double ts = exp(log(scale) + step * dlns);
-        double tc;
-        if (half == 0 && depth_solvable) {
-          // The full step is accepted almost always, and the depth block
-          // then assembles at exactly this (state, scale) and starts from
-          // exactly this cost (fusion.hpp:426-429). So the first trial's
-          // sweep assembles the normal equations speculatively; its cost
-          // is the trial cost, and on acceptance the assembly stands.
-          double v[4];
-          sweep_assemble<SU>(a, sel, rg, a.ld[cur], sel.scale ? log(ts) : 0.0, false, v);
-          grid_allreduce(c, v);  // fenced: the PCG reads the assembled rasters
-          tc = v[3];
-          if (tc <= c0) {
-            have_eq = true;
-            for (int k = 0; k < 4; ++k) veq[k] = v[k];
-          }
-        } else {
-          double v[1] = {sweep_cost<SU>(a, sel, rg, PlainLd{a.ld[cur]},
-                                        sel.scale ? log(ts) : 0.0, nullptr)};
-          DF_OTRACE(5);
-          grid_allreduce<1, false>(c, v);
-          tc = v[0];
-        }
-        if (threadIdx.x == 0) gn_cnt[0] += 1;
-        if (tc <= c0) {
-          scale = ts;
-          accepted = step;
-          break;
-        }
-        step *= 0.5;
-      }
-      if (leader && it < DFUSE_STATS_MAX_GN) ctl->stats.scale_step[it] = accepted;
-      DF_OTRACE(1);
-    }
-    if (depth_solvable) {  // fusion.hpp:426-441
-      const double ln_s = sel.scale ? log(scale) : 0.0;
-      double v[4];
-      if (have_eq) {  // assembled by the accepted scale trial
-        for (int k = 0; k < 4; ++k) v[k] = veq[k];
-      } else {
-        sweep_assemble<SU>(a, sel, rg, a.ld[cur], ln_s, false, v);
-        grid_allreduce(c, v);
-      }
-      const double c0 = v[3];
-      if (threadIdx.x == 0) gn_cnt[0] += 1;
-      DF_OTRACE(2);
-      int its = 0;
-      if (v[0] != 0.0) {
-        if (v[2] > 0.0) {
-          status = DFUSE_E_CG_DIVERGENCE;
-        } else {
-          status = pcg_solve<PPT, VAR>(c, a, rg, v[0], v[1], &its);
-        }
-      }
-      DF_OTRACE(3);
-      if (threadIdx.x == 0) gn_cnt[1] += its;
-      if (leader && it < DFUSE_STATS_MAX_GN) ctl->stats.pcg_iters[it] = its;
-      if (status) break;
-      double step = 1.0, accepted = 0.0;
-      const bool xzero = its == 0;  // delta == 0 (b == 0 or cg_max_iters == 0)
-      for (int half = 0; half <= 5; ++half) {
-        double w[1];
-        if (xzero)
-          w[0] = sweep_cost<SU>(a, sel, rg, PlainLd{a.ld[cur]}, ln_s, a.ld[1 - cur]);
-        else
-          w[0] = sweep_cost<SU>(a, sel, rg, TrialLd{a.ld[cur], a.x, step}, ln_s, a.ld[1 - cur]);
-        DF_OTRACE(6);
-        grid_allreduce(c, w);
-        if (threadIdx.x == 0) gn_cnt[0] += 1;
-        if (w[0] <= c0) {
-          cur = 1 - cur;
-          accepted = step;
-          break;
-        }
-        step *= 0.5;
-      }
-      if (leader && it < DFUSE_STATS_MAX_GN) ctl->stats.depth_step[it] = accepted;
-      DF_OTRACE(4);
-    }
-    if (threadIdx.x == 0) gn_cnt[2] = it + 1;  // gn_done; iteration += 1 (fusion.hpp:442)
-  }
-#undef DF_OTRACE
-  if (otr)
-    for (int k = 0; k < 7; ++k) ctl->trace[8 + k] = ot[k];
-  if (status == 0 && ls_mode) {  // fusion.hpp:445-452
-    double v[1] = {0.0};
-    const double* ld = a.ld[cur];
-    for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) v[0] += a.pred[0][i] - ld[i];
-    grid_allreduce(c, v);
-    const double offset = v[0] / (double)((long)a.W * a.H);
-    double* ldw = a.ld[cur];
-    for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) {
-      ldw[i] += offset;
-      halo_put(a, cur ? HP_LD1 : HP_LD0, i, ldw[i]);
-    }
-    scale = exp(offset);
-  }
-  if (leader) {
-    FusionStateDev out = *a.st_in;  // transactional: unchanged on error
-    if (status == 0) {
-      out.scale = scale;
-      out.iteration += gn_cnt[2];
-      out.cur = cur;
-    }
-    *a.st_out = out;
-    ctl->scale = out.scale;
-    ctl->iteration = out.iteration;
-    ctl->ld_final = out.cur;
-    ctl->stats.gn_done = gn_cnt[2];
-    ctl->stats.pcg_total = gn_cnt[1];
-    ctl->stats.cost_evals = gn_cnt[0];
-  }
-}
-
-// PPT: pixels per thread of the SM-resident PCG (0 = streaming PCG);
-// VAR: resident PCG variant (0 pipelined, 1 Chronopoulos-Gear, 2 two
-// all-reduces). One instantiation per (PPT, VAR) keeps each kernel's code
-// and register allocation to the one PCG loop it runs.
-template <int PPT, int VAR>
-__global__ void __launch_bounds__(FT, 1) k_fusion(FusionArgs a) {
-  constexpr int SU = PPT > 0 ? PPT : 2;  // pixels per thread per unrolled sweep group
-  GridCtx c{a.slots, gridDim.x, a.base_tag, 0u, 0, 1u};
-  const Range rg = my_range(a);
-  const Sel sel = terms_for(a.mode);
-  FusionControl* ctl = a.ctl;
-  const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
-  int status = 0;
-  if (blockIdx.x == 0) {  // only CTA 0 (its thread 0) writes ctl afterwards
-    for (int k = threadIdx.x; k < DFUSE_STATS_MAX_GN; k += FT) {
-      ctl->stats.pcg_iters[k] = -1;
-      ctl->stats.scale_step[k] = -1.0;
-      ctl->stats.depth_step[k] = -1.0;
-    }
-    if (threadIdx.x < 16) ctl->trace[threadIdx.x] = 0;
-    __syncthreads();
-  }
-  if (a.op != OP_PCG) {
-    sweep_prologue(a, rg);
-    grid_sync(c);  // fenced: sweeps read the per-call planes at i-1 and i-W
-  }
-
-  if (a.op == OP_COST) {
-    double v[1] = {sweep_cost<SU>(a, sel, rg, PlainLd{a.ld[0]}, sel.scale ? log(a.scale0) : 0.0,
-                              nullptr)};
-    grid_allreduce(c, v);
-    if (leader) ctl->value[0] = v[0];
-  } else if (a.op == OP_ASSEMBLE) {
-    double v[4];
-    sweep_assemble<SU>(a, sel, rg, a.ld[0], sel.scale ? log(a.scale0) : 0.0, true, v);
-  } else if (a.op == OP_SCALE) {
-    double ln_s = log(a.scale0);  // fusion.hpp:377
-    for (int round = 0; round < 3; ++round) {
-      double v[4];
-      sweep_scale<SU>(a, sel, rg, a.ld[0], ln_s, false, 0.0, v);
-      double w[2] = {v[0], v[1]};
-      grid_allreduce(c, w);
-      ln_s = w[0] / w[1];
-    }
-    if (leader) ctl->value[0] = exp(ln_s);
-  } else if (a.op == OP_PCG) {
-    double v[4];
-    sweep_pcg_init(a, rg, v);
-    double w[3] = {v[0], v[1], v[2]};
-    grid_allreduce(c, w);
-    int its = 0;
-    if (w[0] == 0.0) {
-      sweep_zero_x(a, rg);
-    } else if (w[2] > 0.0) {
-      status = DFUSE_E_CG_DIVERGENCE;
-    } else {
-      status = pcg_solve<PPT, VAR>(c, a, rg, w[0], w[1], &its);
-      // diagnostics (DFUSE_PCG_REPEAT=n[,sweep]): solve the same system n-1
-      // more times in this launch, optionally after a streaming sweep
-      for (int rep = 1; rep < a.diag_repeat && status == 0; ++rep) {
-        if (a.diag_sweep) {
-          for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT)
-            a.q[i] = a.diag[i] * a.right[i] + a.down[i] * a.b[i];
-          grid_sync(c);
-        }
-        status = pcg_solve<PPT, VAR>(c, a, rg, w[0], w[1], &its);
-      }
-    }
-    if (leader) ctl->pcg_last = its;
-  } else {  // OP_OPTIMIZE, fusion.hpp:402-454
-    optimize_body<PPT, VAR>(c, a, rg, sel, leader, status);
-  }
-  if (leader) {
-    ctl->status = status;
-    ctl->stats.grid_syncs = c.syncs;
-  }
-}
 
 // optimize() over row bands: CTAs [b cpr, (b+1) cpr)
 // of this launch run band band0 + b with that band's FusionArgs, the
@@ -1419,20 +184,17 @@ static unsigned long long next_tag() {
   return (__atomic_add_fetch(&seq, 1ULL, __ATOMIC_RELAXED)) << 32;
 }
 
-constexpr size_t kMaxDynSmem = 227 * 1024;
+constexpr size_t kMaxDynSmem = 227 * 1024;  // also in fusion_launch.cuh
 
 int fusion_grid(dfuse_ctx* ctx) {
   static int occ = -1;
   if (occ < 0) {
-    int o[5] = {0, 0, 0, 0, 0};
-    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[0], k_fusion<0, 0>, FT, 0));
-    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[1], k_fusion<4, 0>, FT, 0));
-    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[2], k_fusion<5, 0>, FT, 0));
-    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[3], k_fusion<6, 0>, FT, 0));
-    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[4], k_gradient, FT, 0));
-    occ = o[0];
-    for (int k = 1; k < 5; ++k)
-      if (o[k] < occ) occ = o[k];
+    // every grid-synchronising kernel is __launch_bounds__(FT, 1); these two
+    // stand for the k_fusion instantiations of the fusion_part_*.cu units
+    int o[2] = {0, 0};
+    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[0], k_fusion_banded, FT, 0));
+    DF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o[1], k_gradient, FT, 0));
+    occ = o[0] < o[1] ? o[0] : o[1];
     if (occ < 1) throw CudaFailure{cudaErrorLaunchOutOfResources, "k_fusion occupancy"};
   }
   int g = ctx->solver_ctas > 0 ? ctx->solver_ctas : ctx->num_sms;
@@ -1482,23 +244,6 @@ void plan_tiles(FusionArgs& a, int grid) {
   // LL flags are 32-bit: the whole launch must fit
   if ((double)a.gn * ((double)a.cg_max + 2.0) > 2.0e9) a.ppt = 0;
   if (!a.halo) a.ppt = 0;
-}
-
-template <int PPT, int VAR = 0>
-static void launch_fusion_t(dfuse_ctx* ctx, FusionArgs& a, int grid) {
-  size_t smem = 0;
-  if (PPT > 0) {
-    smem = pcg_tile_smem(PPT, a.tw_max, a.th_max);
-    static size_t configured = 0;
-    if (smem > configured) {
-      DF_CUDA(cudaFuncSetAttribute((const void*)k_fusion<PPT, VAR>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      configured = smem;
-    }
-  }
-  void* args[] = {&a};
-  DF_CUDA(cudaLaunchCooperativeKernel((const void*)k_fusion<PPT, VAR>, dim3(grid), dim3(FT), args,
-                                      smem, ctx->stream));
 }
 
 void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {

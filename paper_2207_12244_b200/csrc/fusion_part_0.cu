@@ -1,0 +1,6 @@
+// fusion_part_0.cu -- k_fusion instantiations <0, 0> (see fusion_impl.cuh)
+#include "fusion_launch.cuh"
+
+namespace dfuse_cuda {
+template void launch_fusion_t<0, 0>(dfuse_ctx*, FusionArgs&, int);
+}  // namespace dfuse_cuda

@@ -1,0 +1,8 @@
+// fusion_part_4.cu -- k_fusion instantiations <4, 0>, <4, 1>, <4, 2> (see fusion_impl.cuh)
+#include "fusion_launch.cuh"
+
+namespace dfuse_cuda {
+template void launch_fusion_t<4, 0>(dfuse_ctx*, FusionArgs&, int);
+template void launch_fusion_t<4, 1>(dfuse_ctx*, FusionArgs&, int);
+template void launch_fusion_t<4, 2>(dfuse_ctx*, FusionArgs&, int);
+}  // namespace dfuse_cuda
