@@ -259,9 +259,12 @@ void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
   }
   a.base_tag = next_tag();
   // LL flags restart at 1 every launch: clear the slots and the halo words
-  DF_CUDA(cudaMemsetAsync(a.slots, 0, fusion_slots_bytes(grid), ctx->stream));
-  if (a.ppt > 0)
-    DF_CUDA(cudaMemsetAsync(a.halo, 0, fusion_halo_bytes((long)a.W * a.H), ctx->stream));
+  // (a session's launches continue the flags instead, FusionArgs::persist_sync)
+  if (!a.persist_sync) {
+    DF_CUDA(cudaMemsetAsync(a.slots, 0, fusion_slots_bytes(grid), ctx->stream));
+    if (a.ppt > 0)
+      DF_CUDA(cudaMemsetAsync(a.halo, 0, fusion_halo_bytes((long)a.W * a.H), ctx->stream));
+  }
   a.trace = ctx->trace;
   a.diag_repeat = ctx->diag_repeat;
   a.diag_sweep = ctx->diag_sweep;

@@ -30,6 +30,10 @@ struct FusionControl {
   double scale;
   double value[2];
   long long trace[16];  // SM cycles per phase, CTA 0 (DFUSE_TRACE=1)
+  // all-reduce phase and LL flag counters carried from one launch to the next
+  // (FusionArgs::persist_sync): flags keep growing, so no launch has to clear
+  // the slot and halo words the previous one left behind
+  unsigned sync_phase, sync_ll;
   dfuse_solver_stats stats;
 };
 
@@ -81,6 +85,7 @@ struct FusionArgs {
   int pcg_variant;  // resident PCG: 0 pipelined (default), 1 Chronopoulos-Gear, 2 two all-reduces
   int trace;  // record per-phase cycle counts of the resident PCG in ctl->trace
   int stage_n;  // > 0: scale rounds 1-2 read round 0's values from shared memory
+  int persist_sync;  // continue the LL flags of ctl (no per-launch clearing)
   long long* dbg;  // DFUSE_TRACE=2: per-CTA phase times [grid][8]
   FusionControl* ctl;
   // row band (banded launches; otherwise y0 = 0, y1 = H, ctas = 0 = the grid)

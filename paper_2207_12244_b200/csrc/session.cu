@@ -67,6 +67,17 @@ int kf_guarded(dfuse_keyframe* kf, F&& f) {
 
 size_t al(size_t v) { return (v + 255) & ~size_t(255); }
 
+// slot and halo words of the all-reduces and the LL counters, cleared once:
+// the session's launches then continue the flags (FusionArgs::persist_sync)
+void clear_sync(dfuse_keyframe* kf) {
+  dfuse_ctx* ctx = kf->ctx;
+  FusionArgs& f = kf->fa;
+  DF_CUDA(cudaMemsetAsync(f.slots, 0, fusion_slots_bytes(kf->grid), ctx->stream));
+  if (f.halo) DF_CUDA(cudaMemsetAsync(f.halo, 0, fusion_halo_bytes(kf->P), ctx->stream));
+  DF_CUDA(cudaMemsetAsync(f.ctl, 0, sizeof(FusionControl), ctx->stream));
+  f.persist_sync = 1;
+}
+
 void reset_state(dfuse_keyframe* kf) {
   dfuse_ctx* ctx = kf->ctx;
   const long P = kf->P;
@@ -139,6 +150,8 @@ void process(dfuse_keyframe* kf, const dfuse_epigeom* g, const float* I1_dev,
                           ctx->stream));
   DF_CUDA(cudaStreamSynchronize(ctx->stream));
   kf->parity = 1 - kf->parity;
+  if (kf->h_ctl->sync_phase > (1u << 30) || kf->h_ctl->sync_ll > (1u << 30))
+    clear_sync(kf);  // 32-bit LL flags: start over long before they wrap
   const int n_obs = kf->h_counters[2];
   if (n_obs > 0) kf->stereo_frames += 1;  // pipeline.hpp:211
   res->observations = n_obs;
@@ -222,6 +235,7 @@ void kf_finish(dfuse_keyframe* kf, const float* I0, double texture_threshold) {
   launch_mask_list(ctx, kf->mask, P, kf->list, kf->counters + 1);
   DF_CUDA(cudaMemcpyAsync(&kf->n_mask, kf->counters + 1, sizeof(int), cudaMemcpyDeviceToHost,
                           ctx->stream));
+  clear_sync(kf);
   reset_state(kf);  // synchronises
 }
 
