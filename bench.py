@@ -336,7 +336,24 @@ def main():
 
     for _ in range(max(3, args.warmup)):
         step()
-    # ---------------- device-timed region
+    # ---------------- per-frame statistics: one synchronous pass over the
+    # keyframe's frames (the computation is deterministic, so the timed pass
+    # below repeats exactly these frames)
+    kf.reset()
+    counter[0] = 0
+    stats_pass = [step() for _ in range(nF)]
+    # ---------------- device-timed region: frames enqueued back to back
+    # (process_frame_async where the keyframe has it; the row-band form is
+    # synchronous), per-step CUDA events on the library's stream
+    use_async = hasattr(kf, "process_frame_async") and not isinstance(kf, api.BandedKeyframe)
+
+    def step_async():
+        k = counter[0] % nF
+        if k == 0 and counter[0] > 0:
+            kf.reset()
+        counter[0] += 1
+        kf.process_frame_async(geoms[k], dev_frames[k].data_ptr(), spec.search, cfg, "full")
+
     kf.reset()
     counter[0] = 0
     if ws > 1:
@@ -345,25 +362,30 @@ def main():
     launches0 = ctx.launch_count()
     sampler = ClockSampler(device)
     sampler.start()
-    step_ms, fusion_ms, stereo_ms, fusion_bytes, pcg, obs = [], [], [], [], [], []
+    events = []
     with torch.cuda.stream(stream):
         for _ in range(args.steps):
             flush.fill_(float(counter[0]))  # evict L2 (outside the events)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            res = step()
+            if use_async:
+                step_async()
+            else:
+                step()
             e1.record(stream)
-            e1.synchronize()
-            step_ms.append(e0.elapsed_time(e1))
-            fusion_ms.append(res.optimise_ms)
-            stereo_ms.append(res.stereo_ms)
-            fusion_bytes.append(fusion_bytes_per_px(res.stats) * P)
-            pcg.append(res.stats.pcg_total)
-            obs.append(res.observations)
+            events.append((e0, e1))
+        if use_async:
+            kf.last_result()
     torch.cuda.synchronize(device)
     clocks = sampler.stop()
     launches = ctx.launch_count() - launches0
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in events]
+    fusion_ms = [r.optimise_ms for r in stats_pass]
+    stereo_ms = [r.stereo_ms for r in stats_pass]
+    fusion_bytes = [fusion_bytes_per_px(r.stats) * P for r in stats_pass]
+    pcg = [r.stats.pcg_total for r in stats_pass]
+    obs = [r.observations for r in stats_pass]
     total_ms = float(np.sum(step_ms))
     if ws > 1:
         t = torch.tensor([total_ms], device=f"cuda:{device}", dtype=torch.float64)
@@ -421,7 +443,9 @@ def main():
                    "l2": "flushed before every step (512 MiB write)"},
         "mpix_per_s": round(value * P / 1e6, 4),
         "stage_ms": {"stereo": round(float(np.mean(stereo_ms)), 4),
-                     "optimise": round(float(np.mean(fusion_ms)), 4)},
+                     "optimise": round(float(np.mean(fusion_ms)), 4),
+                     "source": "one synchronous pass over the keyframe's frames"},
+        "submission": "async (frames enqueued back to back)" if use_async else "synchronous",
         "pcg_iters_per_update": round(float(np.mean(pcg)), 2),
         "observations_per_update": round(float(np.mean(obs)), 1),
         "roofline": {"kernel": "k_fusion", "bound": "hbm", "achieved": round(achieved, 2),

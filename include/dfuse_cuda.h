@@ -346,7 +346,8 @@ int dfuse_kf_score(dfuse_keyframe* kf, const double* gt_metres, const uint8_t* g
  * round(exp(log_depth) * depth_scale) clamped to [0, 65535]
  * (eval.hpp:221-226, depth_io.hpp:51-63); PNG encoding is the caller's */
 int dfuse_kf_export_depth_u16(dfuse_keyframe* kf, double depth_scale, uint16_t* out);
-/* restore the just-created state (device-to-device copies) */
+/* restore the just-created state (device-to-device copies, enqueued on the
+ * context's stream like every later call) */
 int dfuse_kf_reset(dfuse_keyframe* kf);
 /* process_frame for a tracked frame: stereo scan + update + optimize.
  * I1 is a host image (copied in); _dev takes a device pointer. */
@@ -356,6 +357,15 @@ int dfuse_kf_process_frame(dfuse_keyframe* kf, const dfuse_epigeom* g, const flo
 int dfuse_kf_process_frame_dev(dfuse_keyframe* kf, const dfuse_epigeom* g, const float* I1_dev,
                                const dfuse_search_cfg* scfg, const dfuse_robust_cfg* rcfg,
                                int mode, dfuse_frame_result* res);
+/* The same for a device image, enqueued on the context's stream without
+ * waiting: frames can be submitted back to back (the next frame's stereo
+ * uses this frame's semi-dense update, stream order keeps that).
+ * dfuse_kf_last_result waits for everything enqueued and returns the last
+ * frame's result (stereo_frames counts every enqueued frame). */
+int dfuse_kf_process_frame_async(dfuse_keyframe* kf, const dfuse_epigeom* g,
+                                 const float* I1_dev, const dfuse_search_cfg* scfg,
+                                 const dfuse_robust_cfg* rcfg, int mode);
+int dfuse_kf_last_result(dfuse_keyframe* kf, dfuse_frame_result* res);
 /* copy state back to the host (any pointer may be NULL) */
 int dfuse_kf_download(dfuse_keyframe* kf, double* log_depth, double* scale, int32_t* iteration,
                       double* semi_depth, double* semi_variance, uint8_t* semi_valid,

@@ -56,6 +56,9 @@ def lib() -> C.CDLL:
             f.argtypes = [C.c_void_p, C.POINTER(EpiGeom), C.c_void_p, C.c_void_p, C.c_void_p,
                           C.c_int, C.POINTER(FrameResultC)]
         L.dfuse_kf_download.argtypes = [C.c_void_p] + [C.c_void_p] * 8
+        L.dfuse_kf_process_frame_async.argtypes = [C.c_void_p, C.POINTER(EpiGeom), C.c_void_p,
+                                                   C.c_void_p, C.c_void_p, C.c_int]
+        L.dfuse_kf_last_result.argtypes = [C.c_void_p, C.POINTER(FrameResultC)]
         L.dfuse_kf_create_dfpred.argtypes = [C.c_void_p, C.POINTER(Intrinsics), C.c_void_p,
                                              C.c_char_p, C.c_size_t, C.c_double,
                                              C.POINTER(C.c_void_p)]
@@ -254,6 +257,24 @@ class Keyframe:
         self._check(rc, "dfuse_kf_process_frame")
         return res
 
+    def process_frame_async(self, g: EpiGeom, device_ptr: int,
+                            search: SearchConfig | None = None,
+                            robust: RobustConfig | None = None, mode="full") -> None:
+        """process_frame for a device image, enqueued without waiting
+        (dfuse_kf_process_frame_async); last_result() waits and returns the
+        last enqueued frame's result."""
+        search = search or SearchConfig()
+        robust = robust or RobustConfig()
+        self._sc, self._rc = search.c(), robust.c()  # alive until the call returns
+        self._check(lib().dfuse_kf_process_frame_async(
+            self.handle, C.byref(g), C.c_void_p(device_ptr), C.byref(self._sc),
+            C.byref(self._rc), _mode(mode)), "dfuse_kf_process_frame_async")
+
+    def last_result(self):
+        res = FrameResultC()
+        self._check(lib().dfuse_kf_last_result(self.handle, C.byref(res)), "dfuse_kf_last_result")
+        return res
+
     def download(self):
         """-> (FusionState, SemiDenseMap, mask)"""
         h, w = self.H, self.W
@@ -310,6 +331,9 @@ class BandedKeyframe(Keyframe):
 
     def reset(self):
         self._check(lib().dfuse_bkf_reset(self.handle), "dfuse_bkf_reset")
+
+    def process_frame_async(self, *a, **k):
+        raise NotImplementedError("the row-band keyframe has no asynchronous frame call")
 
     def process_frame(self, g: EpiGeom, I1, search: SearchConfig | None = None,
                       robust: RobustConfig | None = None, mode="full", device_ptr=None):

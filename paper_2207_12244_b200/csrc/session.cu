@@ -26,7 +26,6 @@ struct dfuse_keyframe {
   int W = 0, H = 0;
   long P = 0;
   int n_mask = 0;
-  int stereo_frames = 0;
   int parity = 0;
   int grid = 0;
   void* block = nullptr;  // one device allocation for everything below
@@ -37,12 +36,14 @@ struct dfuse_keyframe {
   double* semi_d = nullptr;
   double* semi_v = nullptr;
   uint8_t* semi_valid = nullptr;
-  int* counters = nullptr;  // [0] work [1] n_list [2] n_obs [3] unused [4] inlier_count
+  int* counters = nullptr;  // [0] work [1] n_list [2] n_obs [3] stereo_frames [4] inlier_count
   FusionArgs fa;
   FusionStateDev* st = nullptr;  // [2] ping-pong
   FusionControl* h_ctl = nullptr;  // pinned
   int* h_counters = nullptr;       // pinned
   double median_depth = -1.0;      // cached median_predicted_depth (< 0: not computed)
+  bool pending = false;            // a frame was enqueued and not yet collected
+  FusionStateDev* h_s0 = nullptr;  // pinned: init_state's scalars for reset
 };
 
 namespace {
@@ -85,21 +86,20 @@ void reset_state(dfuse_keyframe* kf) {
   DF_CUDA(cudaMemsetAsync(kf->semi_d, 0, sizeof(double) * P, ctx->stream));
   DF_CUDA(cudaMemsetAsync(kf->semi_v, 0, sizeof(double) * P, ctx->stream));
   DF_CUDA(cudaMemsetAsync(kf->semi_valid, 0, P, ctx->stream));
-  DF_CUDA(cudaMemsetAsync(kf->counters + 4, 0, sizeof(int), ctx->stream));
+  DF_CUDA(cudaMemsetAsync(kf->counters + 3, 0, 2 * sizeof(int), ctx->stream));
   DF_CUDA(cudaMemcpyAsync(kf->fa.ld[0], kf->fa.pred[0], sizeof(double) * P,
                           cudaMemcpyDeviceToDevice, ctx->stream));
-  FusionStateDev s0{1.0, 0, 0};
   kf->parity = 0;
-  DF_CUDA(cudaMemcpyAsync(kf->st, &s0, sizeof s0, cudaMemcpyHostToDevice, ctx->stream));
-  DF_CUDA(cudaStreamSynchronize(ctx->stream));
-  kf->stereo_frames = 0;
+  DF_CUDA(cudaMemcpyAsync(kf->st, kf->h_s0, sizeof(FusionStateDev), cudaMemcpyHostToDevice,
+                          ctx->stream));
 }
 
-void process(dfuse_keyframe* kf, const dfuse_epigeom* g, const float* I1_dev,
-             const dfuse_search_cfg* scfg, const dfuse_robust_cfg* rcfg, int mode,
-             dfuse_frame_result* res) {
+// process_frame, enqueued on the context's stream (no host synchronisation):
+// the result lands in pinned host memory, read by collect()
+void enqueue(dfuse_keyframe* kf, const dfuse_epigeom* g, const float* I1_dev,
+             const dfuse_search_cfg* scfg, const dfuse_robust_cfg* rcfg, int mode) {
   dfuse_ctx* ctx = kf->ctx;
-  if (!g || !scfg || !rcfg || !res) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null pointer"};
+  if (!g || !scfg || !rcfg) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null pointer"};
   if (g->K.width != kf->W || g->K.height != kf->H)
     throw RefError{DFUSE_E_DIMENSION_MISMATCH, "frame does not match the keyframe raster"};
   if (mode < 0 || mode > 2) throw RefError{DFUSE_E_INVALID_ARGUMENT, "unknown fusion mode"};
@@ -148,15 +148,22 @@ void process(dfuse_keyframe* kf, const dfuse_epigeom* g, const float* I1_dev,
                           ctx->stream));
   DF_CUDA(cudaMemcpyAsync(kf->h_ctl, f.ctl, sizeof(FusionControl), cudaMemcpyDeviceToHost,
                           ctx->stream));
-  DF_CUDA(cudaStreamSynchronize(ctx->stream));
   kf->parity = 1 - kf->parity;
+  kf->pending = true;
+}
+
+// wait for the frames enqueued so far; res = the last one's outcome
+void collect(dfuse_keyframe* kf, dfuse_frame_result* res) {
+  dfuse_ctx* ctx = kf->ctx;
+  if (!res) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null pointer"};
+  if (!kf->pending) throw RefError{DFUSE_E_INVALID_ARGUMENT, "no frame enqueued"};
+  DF_CUDA(cudaStreamSynchronize(ctx->stream));
+  kf->pending = false;
   if (kf->h_ctl->sync_phase > (1u << 30) || kf->h_ctl->sync_ll > (1u << 30))
     clear_sync(kf);  // 32-bit LL flags: start over long before they wrap
-  const int n_obs = kf->h_counters[2];
-  if (n_obs > 0) kf->stereo_frames += 1;  // pipeline.hpp:211
-  res->observations = n_obs;
+  res->observations = kf->h_counters[2];
   res->inlier_count = kf->h_counters[4];
-  res->stereo_frames = kf->stereo_frames;
+  res->stereo_frames = kf->h_counters[3];  // counted on the device, pipeline.hpp:211
   res->optimize_status = kf->h_ctl->status;  // CgDivergence: solve skipped, pipeline.hpp:328-331
   DF_CUDA(cudaEventElapsedTime(&res->stereo_ms, ctx->ev[0], ctx->ev[1]));
   DF_CUDA(cudaEventElapsedTime(&res->optimise_ms, ctx->ev[1], ctx->ev[2]));
@@ -204,6 +211,7 @@ void kf_alloc(dfuse_keyframe* kf, const dfuse_intrinsics* K) {
   f.irs = (double*)take(dP);
   for (int k = 0; k < 3; ++k) f.ivar[k] = (double*)take(dP);
   f.inlier_dev = kf->counters + 4;
+  f.session_counters = kf->counters;
   f.ld[0] = (double*)take(dP);
   f.ld[1] = (double*)take(dP);
   f.diag = (double*)take(dP);
@@ -222,6 +230,8 @@ void kf_alloc(dfuse_keyframe* kf, const dfuse_intrinsics* K) {
   kf->st = (FusionStateDev*)take(2 * sizeof(FusionStateDev));
   DF_CUDA(cudaMallocHost(&kf->h_ctl, sizeof(FusionControl)));
   DF_CUDA(cudaMallocHost(&kf->h_counters, 8 * sizeof(int)));
+  DF_CUDA(cudaMallocHost(&kf->h_s0, sizeof(FusionStateDev)));
+  *kf->h_s0 = FusionStateDev{1.0, 0, 0};  // init_state, fusion.hpp:44-46
   DF_CUDA(cudaMemsetAsync(kf->counters, 0, 256, ctx->stream));
 }
 
@@ -236,7 +246,8 @@ void kf_finish(dfuse_keyframe* kf, const float* I0, double texture_threshold) {
   DF_CUDA(cudaMemcpyAsync(&kf->n_mask, kf->counters + 1, sizeof(int), cudaMemcpyDeviceToHost,
                           ctx->stream));
   clear_sync(kf);
-  reset_state(kf);  // synchronises
+  reset_state(kf);
+  DF_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 void check_kf_args(const dfuse_intrinsics* K, const float* I0, double texture_threshold) {
@@ -458,11 +469,13 @@ int dfuse_kf_destroy(dfuse_keyframe* kf) {
   if (kf->block) cudaFree(kf->block);
   if (kf->h_ctl) cudaFreeHost(kf->h_ctl);
   if (kf->h_counters) cudaFreeHost(kf->h_counters);
+  if (kf->h_s0) cudaFreeHost(kf->h_s0);
   delete kf;
   return DFUSE_OK;
 }
 
 int dfuse_kf_reset(dfuse_keyframe* kf) {
+  // stream-ordered like everything after it: no need to wait here
   return kf_guarded(kf, [&] { reset_state(kf); });
 }
 
@@ -473,7 +486,8 @@ int dfuse_kf_process_frame(dfuse_keyframe* kf, const dfuse_epigeom* g, const flo
     if (!I1) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null image"};
     DF_CUDA(cudaMemcpyAsync(kf->I1, I1, sizeof(float) * kf->P, cudaMemcpyHostToDevice,
                             kf->ctx->stream));
-    process(kf, g, kf->I1, scfg, rcfg, mode, res);
+    enqueue(kf, g, kf->I1, scfg, rcfg, mode);
+    collect(kf, res);
   });
 }
 
@@ -482,8 +496,22 @@ int dfuse_kf_process_frame_dev(dfuse_keyframe* kf, const dfuse_epigeom* g, const
                                int mode, dfuse_frame_result* res) {
   return kf_guarded(kf, [&] {
     if (!I1_dev) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null image"};
-    process(kf, g, I1_dev, scfg, rcfg, mode, res);
+    enqueue(kf, g, I1_dev, scfg, rcfg, mode);
+    collect(kf, res);
   });
+}
+
+int dfuse_kf_process_frame_async(dfuse_keyframe* kf, const dfuse_epigeom* g,
+                                 const float* I1_dev, const dfuse_search_cfg* scfg,
+                                 const dfuse_robust_cfg* rcfg, int mode) {
+  return kf_guarded(kf, [&] {
+    if (!I1_dev) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null image"};
+    enqueue(kf, g, I1_dev, scfg, rcfg, mode);
+  });
+}
+
+int dfuse_kf_last_result(dfuse_keyframe* kf, dfuse_frame_result* res) {
+  return kf_guarded(kf, [&] { collect(kf, res); });
 }
 
 int dfuse_kf_download(dfuse_keyframe* kf, double* log_depth, double* scale, int32_t* iteration,

@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 from paper_2207_12244_b200 import api, synth
-from paper_2207_12244_b200._ffi import RobustConfig, SemiDenseMap, init_state
+from paper_2207_12244_b200._ffi import DfuseError, RobustConfig, SemiDenseMap, init_state
 from helpers import rel_err
 
 pytestmark = pytest.mark.gpu
@@ -52,3 +52,40 @@ def test_launch_counter_moves(gpu_ctx):
     before = gpu_ctx.launch_count()
     gpu_ctx.api.texture_mask(np.zeros((16, 16), np.float32), 0.02)
     assert gpu_ctx.launch_count() > before
+
+
+def test_async_frames_equal_sync_frames(gpu_ctx):
+    """dfuse_kf_process_frame_async: frames enqueued back to back give the
+    state and counts of the synchronous calls, bit for bit (stereo_frames is
+    counted on the device); reset is stream-ordered too."""
+    import torch
+
+    spec = synth.small_spec(160, 120, frames=4)
+    seq = synth.make_sequence(spec, 33, frames=4)
+    cfg = RobustConfig(gn_iterations=3)
+    geoms = [gpu_ctx.api.make_epipolar_geometry(synth.IDENTITY_Q, np.zeros(3), q, t,
+                                                spec.camera()) for (q, t, _) in seq.frames]
+    dev = [torch.from_numpy(np.ascontiguousarray(I1, np.float32)).cuda()
+           for (_, _, I1) in seq.frames]
+    torch.cuda.synchronize()
+    a = api.Keyframe(gpu_ctx, spec.camera(), seq.I0, seq.pred, 0.02)
+    b = api.Keyframe(gpu_ctx, spec.camera(), seq.I0, seq.pred, 0.02)
+    for rep in range(2):
+        for k in range(len(dev)):
+            ra = a.process_frame(geoms[k], None, spec.search, cfg, "full",
+                                 device_ptr=dev[k].data_ptr())
+            b.process_frame_async(geoms[k], dev[k].data_ptr(), spec.search, cfg, "full")
+        rb = b.last_result()
+        assert (ra.observations, ra.inlier_count, ra.stereo_frames) == \
+            (rb.observations, rb.inlier_count, rb.stereo_frames)
+        sa, ma, _ = a.download()
+        sb, mb, _ = b.download()
+        assert sa.log_depth.tobytes() == sb.log_depth.tobytes()
+        assert (sa.scale, sa.iteration) == (sb.scale, sb.iteration)
+        assert ma.depth.tobytes() == mb.depth.tobytes()
+        a.reset()
+        b.reset()
+    with pytest.raises(DfuseError):
+        b.last_result()  # nothing enqueued since the last result
+    a.close()
+    b.close()
