@@ -144,10 +144,6 @@ void enqueue(dfuse_keyframe* kf, const dfuse_epigeom* g, const float* I1_dev,
   f.st_out = kf->st + (1 - kf->parity);
   launch_fusion(ctx, f, kf->grid);
   DF_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
-  DF_CUDA(cudaMemcpyAsync(kf->h_counters, kf->counters, 8 * sizeof(int), cudaMemcpyDeviceToHost,
-                          ctx->stream));
-  DF_CUDA(cudaMemcpyAsync(kf->h_ctl, f.ctl, sizeof(FusionControl), cudaMemcpyDeviceToHost,
-                          ctx->stream));
   kf->parity = 1 - kf->parity;
   kf->pending = true;
 }
@@ -157,6 +153,12 @@ void collect(dfuse_keyframe* kf, dfuse_frame_result* res) {
   dfuse_ctx* ctx = kf->ctx;
   if (!res) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null pointer"};
   if (!kf->pending) throw RefError{DFUSE_E_INVALID_ARGUMENT, "no frame enqueued"};
+  // the last frame's counters and control block (nothing after it on the
+  // stream touches them)
+  DF_CUDA(cudaMemcpyAsync(kf->h_counters, kf->counters, 8 * sizeof(int), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  DF_CUDA(cudaMemcpyAsync(kf->h_ctl, kf->fa.ctl, sizeof(FusionControl), cudaMemcpyDeviceToHost,
+                          ctx->stream));
   DF_CUDA(cudaStreamSynchronize(ctx->stream));
   kf->pending = false;
   if (kf->h_ctl->sync_phase > (1u << 30) || kf->h_ctl->sync_ll > (1u << 30))
