@@ -85,6 +85,11 @@ def ncu_traffic(kernel):
         return None
 
 
+# FP64 issue rate of this GPU, measured (scripts/micro/fp64_rate.cu): 58 DFMA
+# lane-operations per SM per clock, x 148 SMs x 1.965 GHz
+FP64_PEAK_GOPS = round(58 * 148 * 1.965, 1)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -385,6 +390,7 @@ def main():
     stereo_ms = [r.stereo_ms for r in stats_pass]
     fusion_bytes = [fusion_bytes_per_px(r.stats) * P for r in stats_pass]
     pcg = [r.stats.pcg_total for r in stats_pass]
+    steps_ep = [r.epipolar_steps for r in stats_pass]
     obs = [r.observations for r in stats_pass]
     total_ms = float(np.sum(step_ms))
     if ws > 1:
@@ -457,6 +463,17 @@ def main():
                              "per GN step, executed counts) / k_fusion device time; the "
                              "SM-resident solver moves only `traffic` DRAM bytes per launch, so "
                              "frac > 1 = faster than a streaming solver at full HBM bandwidth"},
+        "stereo_roofline": {
+            "kernel": "k_stereo", "bound": "fp64", "unit": "GFP64op/s",
+            "achieved": round(165.0 * float(np.sum(steps_ep)) / (np.sum(stereo_ms) / 1e3) / 1e9, 1),
+            "peak": FP64_PEAK_GOPS,
+            "frac": round(165.0 * float(np.sum(steps_ep)) / (np.sum(stereo_ms) / 1e3) / 1e9
+                          / FP64_PEAK_GOPS, 4),
+            "epipolar_steps_per_update": round(float(np.mean(steps_ep)), 1),
+            "model": "165 FP64 operations per epipolar step (SURVEY 8(a) a6; 11 IEEE divisions "
+                     "counted as one operation each) / stereo stage time",
+            "peak_source": "scripts/micro/fp64_rate.cu on B200: 58 DFMA lane-ops per SM per "
+                           "clock x 148 SMs x 1965 MHz (operations, not FLOP)"},
         "gpu_launches": int(launches),
         "clocks": clocks,
         "e2e": e2e,

@@ -252,6 +252,8 @@ typedef struct {
   float stereo_ms;        /* device time of the stereo stage */
   float optimise_ms;      /* device time of the optimise stage */
   dfuse_solver_stats stats;
+  int64_t epipolar_steps; /* steps of all epipolar searches of the frame
+                             (semidense.hpp:323), for the stereo roofline */
 } dfuse_frame_result;
 
 /* make_keyframe (pipeline.hpp:125-153) minus prediction I/O: uploads I0 and

@@ -43,7 +43,7 @@ struct Band {
   int* list = nullptr;
   int* counters = nullptr;  // [0] work counter, [1] list length, [2] n_obs, [3] inlier count
   int n_mask = 0;
-  int h_counters[2] = {0, 0};
+  int h_counters[4] = {0, 0, 0, 0};  // n_obs, inliers, steps (64-bit)
   double *semi_d = nullptr, *semi_v = nullptr;
   uint8_t* semi_valid = nullptr;
   unsigned long long* rank_slots = nullptr;
@@ -250,6 +250,7 @@ void process_bkf(dfuse_banded_keyframe* kf, const dfuse_epigeom* g, const float*
   for (Band& b : kf->bands) {
     if (!b.local) continue;
     DF_CUDA(cudaMemsetAsync(b.counters + 2, 0, sizeof(int), ctx->stream));  // n_obs
+    DF_CUDA(cudaMemsetAsync(b.counters + 4, 0, 2 * sizeof(int), ctx->stream));  // steps
     if (b.n_mask == 0) continue;
     StereoArgs a;
     memset(&a, 0, sizeof a);
@@ -265,6 +266,7 @@ void process_bkf(dfuse_banded_keyframe* kf, const dfuse_epigeom* g, const float*
     a.valid = b.semi_valid;
     a.n_obs = b.counters + 2;
     a.n_installed = b.counters + 3;
+    a.step_count = reinterpret_cast<unsigned long long*>(b.counters + 4);
     launch_stereo(ctx, a, false);
   }
   DF_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
@@ -302,16 +304,20 @@ void process_bkf(dfuse_banded_keyframe* kf, const dfuse_epigeom* g, const float*
   DF_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
   for (Band& b : kf->bands)
     if (b.local)
-      DF_CUDA(cudaMemcpyAsync(b.h_counters, b.counters + 2, 2 * sizeof(int),
+      DF_CUDA(cudaMemcpyAsync(b.h_counters, b.counters + 2, 4 * sizeof(int),
                               cudaMemcpyDeviceToHost, ctx->stream));
   DF_CUDA(cudaMemcpyAsync(kf->h_ctl, kf->bands[first].fa.ctl, sizeof(FusionControl),
                           cudaMemcpyDeviceToHost, ctx->stream));
   DF_CUDA(cudaStreamSynchronize(ctx->stream));
   int n_obs = 0, inliers = 0;
+  long long steps = 0;
   for (Band& b : kf->bands)
     if (b.local) {
       n_obs += b.h_counters[0];
       inliers += b.h_counters[1];
+      long long st;
+      memcpy(&st, b.h_counters + 2, sizeof st);
+      steps += st;
     }
   kf->parity = 1 - kf->parity;
   // multi-process: these are this rank's bands (the caller sums over ranks)
@@ -323,6 +329,7 @@ void process_bkf(dfuse_banded_keyframe* kf, const dfuse_epigeom* g, const float*
   DF_CUDA(cudaEventElapsedTime(&res->stereo_ms, ctx->ev[0], ctx->ev[1]));
   DF_CUDA(cudaEventElapsedTime(&res->optimise_ms, ctx->ev[1], ctx->ev[2]));
   res->stats = kf->h_ctl->stats;
+  res->epipolar_steps = steps;
 }
 
 }  // namespace

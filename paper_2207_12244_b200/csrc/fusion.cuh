@@ -86,7 +86,7 @@ struct FusionArgs {
   int trace;  // record per-phase cycle counts of the resident PCG in ctl->trace
   int stage_n;  // > 0: scale rounds 1-2 read round 0's values from shared memory
   int persist_sync;  // continue the LL flags of ctl (no per-launch clearing)
-  int* session_counters;  // keyframe session: [2] n_obs of this frame, [3] stereo_frames
+  int* session_counters;  // keyframe session: [1] n_obs of this frame, [5] stereo_frames
   long long* dbg;  // DFUSE_TRACE=2: per-CTA phase times [grid][8]
   FusionControl* ctl;
   // row band (banded launches; otherwise y0 = 0, y1 = H, ctas = 0 = the grid)

@@ -36,7 +36,10 @@ struct dfuse_keyframe {
   double* semi_d = nullptr;
   double* semi_v = nullptr;
   uint8_t* semi_valid = nullptr;
-  int* counters = nullptr;  // [0] work [1] n_list [2] n_obs [3] stereo_frames [4] inlier_count
+  // [0] stereo work counter, [1] n_obs, [2..3] epipolar steps (64-bit): per
+  // frame, cleared by one memset; [4] inlier_count, [5] stereo_frames: per
+  // keyframe. ([1] holds the masked-pixel count while the keyframe is made.)
+  int* counters = nullptr;
   FusionArgs fa;
   FusionStateDev* st = nullptr;  // [2] ping-pong
   FusionControl* h_ctl = nullptr;  // pinned
@@ -86,7 +89,7 @@ void reset_state(dfuse_keyframe* kf) {
   DF_CUDA(cudaMemsetAsync(kf->semi_d, 0, sizeof(double) * P, ctx->stream));
   DF_CUDA(cudaMemsetAsync(kf->semi_v, 0, sizeof(double) * P, ctx->stream));
   DF_CUDA(cudaMemsetAsync(kf->semi_valid, 0, P, ctx->stream));
-  DF_CUDA(cudaMemsetAsync(kf->counters + 3, 0, 2 * sizeof(int), ctx->stream));
+  DF_CUDA(cudaMemsetAsync(kf->counters + 4, 0, 2 * sizeof(int), ctx->stream));
   DF_CUDA(cudaMemcpyAsync(kf->fa.ld[0], kf->fa.pred[0], sizeof(double) * P,
                           cudaMemcpyDeviceToDevice, ctx->stream));
   kf->parity = 0;
@@ -111,8 +114,7 @@ void enqueue(dfuse_keyframe* kf, const dfuse_epigeom* g, const float* I1_dev,
   }
   // ---- stereo stage: stereo_scan + update_semidense, pipeline.hpp:205-213
   DF_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
-  DF_CUDA(cudaMemsetAsync(kf->counters, 0, sizeof(int), ctx->stream));
-  DF_CUDA(cudaMemsetAsync(kf->counters + 2, 0, sizeof(int), ctx->stream));
+  DF_CUDA(cudaMemsetAsync(kf->counters, 0, 4 * sizeof(int), ctx->stream));
   StereoArgs a;
   memset(&a, 0, sizeof a);
   a.g = *g;
@@ -125,8 +127,9 @@ void enqueue(dfuse_keyframe* kf, const dfuse_epigeom* g, const float* I1_dev,
   a.depth = kf->semi_d;
   a.variance = kf->semi_v;
   a.valid = kf->semi_valid;
-  a.n_obs = kf->counters + 2;
+  a.n_obs = kf->counters + 1;
   a.n_installed = kf->counters + 4;  // inlier_count += newly installed pixels
+  a.step_count = reinterpret_cast<unsigned long long*>(kf->counters + 2);
   if (kf->n_mask > 0) launch_stereo(ctx, a, false);
   DF_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
   // ---- optimise stage, pipeline.hpp:223-226
@@ -163,9 +166,12 @@ void collect(dfuse_keyframe* kf, dfuse_frame_result* res) {
   kf->pending = false;
   if (kf->h_ctl->sync_phase > (1u << 30) || kf->h_ctl->sync_ll > (1u << 30))
     clear_sync(kf);  // 32-bit LL flags: start over long before they wrap
-  res->observations = kf->h_counters[2];
+  res->observations = kf->h_counters[1];
   res->inlier_count = kf->h_counters[4];
-  res->stereo_frames = kf->h_counters[3];  // counted on the device, pipeline.hpp:211
+  res->stereo_frames = kf->h_counters[5];  // counted on the device, pipeline.hpp:211
+  long long steps;
+  memcpy(&steps, kf->h_counters + 2, sizeof steps);
+  res->epipolar_steps = steps;
   res->optimize_status = kf->h_ctl->status;  // CgDivergence: solve skipped, pipeline.hpp:328-331
   DF_CUDA(cudaEventElapsedTime(&res->stereo_ms, ctx->ev[0], ctx->ev[1]));
   DF_CUDA(cudaEventElapsedTime(&res->optimise_ms, ctx->ev[1], ctx->ev[2]));

@@ -26,6 +26,7 @@ struct StereoArgs {
   uint8_t* valid;
   int* n_obs;
   int* n_installed;
+  unsigned long long* step_count;  // optional: epipolar steps of all searches
   // list mode: pixels and optional priors
   const double* px;
   const double* prior;
