@@ -266,6 +266,13 @@ void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
       DF_CUDA(cudaMemsetAsync(a.halo, 0, fusion_halo_bytes((long)a.W * a.H), ctx->stream));
   }
   a.trace = ctx->trace;
+  if (ctx->trace && !DFUSE_TRACE_BUILD) {
+    static bool told = false;
+    if (!told)
+      fprintf(stderr, "dfuse: DFUSE_TRACE needs the diagnostics build (make -C "
+                      "paper_2207_12244_b200/csrc diag; DFUSE_LIB=.../libdfuse_cuda_diag.so)\n");
+    told = true;
+  }
   a.diag_repeat = ctx->diag_repeat;
   a.diag_sweep = ctx->diag_sweep;
   a.dbg = nullptr;

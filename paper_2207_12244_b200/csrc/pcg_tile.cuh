@@ -213,7 +213,7 @@ struct PcgTrace {
     return s;
   }
   __device__ __forceinline__ explicit PcgTrace(const FusionArgs& a, bool resume = false)
-      : on(a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || a.trace == 2)) {
+      : on(DFUSE_TRACE_BUILD && a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || a.trace == 2)) {
     if (on && !resume) {
       long long* s = st();
       for (int k = 0; k < 6; ++k) s[k] = 0;

@@ -1,4 +1,6 @@
-"""Diagnostics: per-phase trace (DFUSE_TRACE=1) of the C2 optimize in the
+"""Run with DFUSE_LIB=paper_2207_12244_b200/libdfuse_cuda_diag.so (make -C
+paper_2207_12244_b200/csrc diag).
+Diagnostics: per-phase trace (DFUSE_TRACE=1) of the C2 optimize in the
 fixed-effort regime (10 GN x 5 PCG iterations)."""
 import os
 import sys

@@ -1,4 +1,6 @@
-"""Diagnostics: per-phase trace (DFUSE_TRACE=1, printed by the library on
+"""Run with DFUSE_LIB=paper_2207_12244_b200/libdfuse_cuda_diag.so (make -C
+paper_2207_12244_b200/csrc diag).
+Diagnostics: per-phase trace (DFUSE_TRACE=1, printed by the library on
 stderr) of the C2 optimize for a few tracked frames on one solver path."""
 import os
 import sys
