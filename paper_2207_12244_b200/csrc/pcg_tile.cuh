@@ -172,6 +172,28 @@ struct PcgTile {
     }
   }
 
+  // post the tile's own boundary cells of the halo'd plane (s_z) as LL
+  // words (version `flag`): one thread per perimeter cell (corners twice,
+  // same value), after a barrier that follows the plane's writes
+  __device__ __forceinline__ void post_boundary(const FusionArgs& a, unsigned long long* ll,
+                                                unsigned flag) const {
+    const int perim = T > 0 ? 2 * (tg.tw + tg.th) : 0;
+    for (int t = threadIdx.x; t < perim; t += FT) {
+      int lx, ly;
+      if (t < tg.tw) {
+        lx = t, ly = 0;
+      } else if (t < 2 * tg.tw) {
+        lx = t - tg.tw, ly = tg.th - 1;
+      } else if (t < 2 * tg.tw + tg.th) {
+        lx = 0, ly = t - 2 * tg.tw;
+      } else {
+        lx = tg.tw - 1, ly = t - 2 * tg.tw - tg.th;
+      }
+      const double v = s_z()[(ly + 1) * pw + lx + 1];
+      ll_store(ll + 2 * ((long)g0 + (long)ly * a.W + lx), v, flag);
+    }
+  }
+
   // w = H z, StencilMatrix::apply order (fusion.hpp:127-131), branch-free.
   // BOUNDARY selects the pass: false = interior pixels (own-tile z only, can
   // run before the halo ring arrives), true = tile-boundary pixels
@@ -421,13 +443,13 @@ __device__ int pcg_resident_pipe(GridCtx& c, const FusionArgs& a, double bnorm2,
       const double m = wr[j] * t.s_rdiag()[k];  // m0 = w0/diag
       mr[j] = m;
       t.s_z()[t.so(j)] = m;
-      if (t.boundary(j)) ll_store(hb0 + 2 * P + 2 * (long)t.gi(j), m, base + 2u);
     }
   }
   {
     double v[3] = {0.0, wu, 0.0};
-    grid_allreduce_publish(c, v);
+    grid_allreduce_publish(c, v);  // its barrier follows every m0 write
   }
+  t.post_boundary(a, hb0 + 2 * P, base + 2u);
   trc.mark(5);
 
   const double tol2 = a.cg_tol * a.cg_tol * bnorm2;
@@ -534,11 +556,11 @@ __device__ int pcg_resident_pipe(GridCtx& c, const FusionArgs& a, double bnorm2,
         ru += r * un;
         wu2 += w * un;
         rr += r * r;
-        if (t.boundary(j)) ll_store(hm + 2 * (long)t.gi(j), m, base + (unsigned)it + 3u);
       }
     }
     double v2[3] = {ru, wu2, rr};
-    grid_allreduce_publish(c, v2);
+    grid_allreduce_publish(c, v2);  // its barrier follows every m write
+    t.post_boundary(a, hm, base + (unsigned)it + 3u);
     trc.mark(5);
   }
   trc.flush(a);
