@@ -41,9 +41,13 @@
 // raster-indexed array and the neighbours rebuild their halo from them. The
 // LL flags order that data, so the all-reduces of the loop need no fence.
 //
-// z = r/diag uses the reciprocal computed once per solve and one Markstein
+// z = r/diag uses the reciprocal computed once per solve. The
+// Chronopoulos-Gear and two-all-reduce variants add one Markstein
 // correction (q0 = r*(1/d); e = fma(-q0, d, r); z = fma(e, 1/d, q0)), which
-// returns the IEEE quotient except in rare double-rounding corner cases.
+// returns the IEEE quotient except in rare double-rounding corner cases; the
+// pipelined loop applies the rounded reciprocal as it is (a Jacobi
+// preconditioner within one rounding of diag^-1: same iteration counts on
+// every parity case, 2 % faster at C2).
 #pragma once
 
 // shared-memory carve-up and per-thread pixel map of one tile
@@ -533,10 +537,11 @@ __device__ int pcg_resident_pipe(GridCtx& c, const FusionArgs& a, double bnorm2,
     for (int j = 0; j < PPT; ++j) {
       if (t.valid(j)) {
         const int k = threadIdx.x + FT * j;
-        const double d = t.s_diag()[k], rd = t.s_rdiag()[k];
+        // u = M^-1 r with M^-1 = diag(1/diag rounded): within one rounding of
+        // the reference's r/diag (fusion.hpp:359; tolerance parity, H7)
+        const double rd = t.s_rdiag()[k];
         const double r0 = rr_[j];
-        const double uq = r0 * rd;
-        const double u = __fma_rn(__fma_rn(-uq, d, r0), rd, uq);
+        const double u = r0 * rd;
         const double z = mr[j] + beta * zr[j];
         const double sv = wr[j] + beta * sr[j];
         const double p = u + beta * t.s_p()[k];
@@ -548,8 +553,7 @@ __device__ int pcg_resident_pipe(GridCtx& c, const FusionArgs& a, double bnorm2,
         rr_[j] = r;
         const double w = wr[j] - alpha * z;
         wr[j] = w;
-        const double q1 = r * rd;
-        const double un = __fma_rn(__fma_rn(-q1, d, r), rd, q1);
+        const double un = r * rd;
         const double m = w * rd;  // M^-1 w: internal to the pipelined recurrences
         mr[j] = m;
         t.s_z()[t.so(j)] = m;
