@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--solver-ctas", type=int, default=0,
+                    help="persistent CTAs of the fusion solver (0 = the library's choice)")
     ap.add_argument("--bands", type=int, default=0,
                     help="row bands of one keyframe (C4 form); under torchrun with --config C4 "
                          "each rank computes one band (strong scaling)")
@@ -306,6 +308,8 @@ def main():
     cfg = solver_cfg(spec, args.regime)
     ctx = api.context(device)
     ctx.set_solver_path(args.solver_path)
+    if args.solver_ctas:
+        ctx.set_solver_ctas(args.solver_ctas)
     if split:
         from paper_2207_12244_b200.bands_dist import DistributedBandedKeyframe
 
