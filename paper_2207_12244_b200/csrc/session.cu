@@ -130,7 +130,7 @@ void enqueue(dfuse_keyframe* kf, const dfuse_epigeom* g, const float* I1_dev,
   a.n_obs = kf->counters + 1;
   a.n_installed = kf->counters + 4;  // inlier_count += newly installed pixels
   a.step_count = reinterpret_cast<unsigned long long*>(kf->counters + 2);
-  if (kf->n_mask > 0) launch_stereo(ctx, a, false);
+  if (kf->n_mask > 0) launch_stereo(ctx, a, false, true);  // counters[0] cleared above
   DF_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
   // ---- optimise stage, pipeline.hpp:223-226
   FusionArgs& f = kf->fa;

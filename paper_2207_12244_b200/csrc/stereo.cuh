@@ -46,7 +46,9 @@ void launch_texture_mask(dfuse_ctx* ctx, const float* img, int w, int h, double 
 // list = indices i (+ index_offset) of the set mask[i], i < P, in any order
 void launch_mask_list(dfuse_ctx* ctx, const uint8_t* mask, long P, int* list, int* count,
                       long index_offset = 0);
-void launch_stereo(dfuse_ctx* ctx, const StereoArgs& a, bool list_mode);
+// counter_zeroed: the caller already cleared a.work_counter on the stream
+void launch_stereo(dfuse_ctx* ctx, const StereoArgs& a, bool list_mode,
+                   bool counter_zeroed = false);
 void launch_count_valid(dfuse_ctx* ctx, const uint8_t* valid, long P, int* out);
 void launch_compact_obs(dfuse_ctx* ctx, const uint8_t* flag, const dfuse_obs* dense, long P,
                         int* block_scratch, dfuse_obs* out);

@@ -89,3 +89,28 @@ def test_async_frames_equal_sync_frames(gpu_ctx):
         b.last_result()  # nothing enqueued since the last result
     a.close()
     b.close()
+
+
+def test_session_c5_stress_matches_oracle(gpu_ctx, orc):
+    """C5: 30 % textureless regions, Laplace priors, search range 0.1-20 m:
+    the semi-dense map bit-exact and the fused state within tolerance for
+    two tracked frames."""
+    spec = synth.CONFIGS["C5"]
+    seq = synth.make_sequence(spec, 41, frames=2)
+    cfg = RobustConfig(gn_iterations=4)
+    kf = api.Keyframe(gpu_ctx, spec.camera(), seq.I0, seq.pred, 0.02)
+    _, _, mask = kf.download()
+    o_semi = SemiDenseMap.empty(spec.width, spec.height)
+    for (q, t, I1) in seq.frames:
+        g = orc.make_epipolar_geometry(synth.IDENTITY_Q, np.zeros(3), q, t, spec.camera())
+        before, _, _ = kf.download()
+        res = kf.process_frame(g, I1, spec.search, cfg, "full")
+        o_semi = orc.stereo_update(g, seq.I0, I1, mask, o_semi, spec.search).semi
+        g_st, g_semi, _ = kf.download()
+        assert g_semi.depth.tobytes() == o_semi.depth.tobytes()
+        assert res.inlier_count == o_semi.inlier_count
+        o_st, so = orc.optimize(before, o_semi, seq.pred, cfg, with_stats=True)
+        assert rel_err(np.exp(g_st.log_depth), np.exp(o_st.log_depth)) < 1e-4
+        assert rel_err(g_st.scale, o_st.scale) < 1e-4
+        assert abs(res.stats.pcg_total - so.pcg_total) <= max(2, 0.02 * so.pcg_total)
+    kf.close()
