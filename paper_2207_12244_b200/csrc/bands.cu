@@ -373,7 +373,10 @@ void create_bkf(dfuse_banded_keyframe* kf, const dfuse_intrinsics* K, const floa
   kf->P = (long)kf->W * kf->H;
   kf->nband = bands;
   kf->rank = rank;
-  kf->cpr = fusion_grid(ctx) / per_process;  // CTAs per band (one per SM overall)
+  // CTAs per band: two per SM overall, like the streaming kernel (whose
+  // reductions a one-band keyframe then reproduces bit for bit)
+  kf->cpr = 2 * fusion_grid(ctx) / per_process;
+  if (kf->cpr > 32 * 5 * 2) kf->cpr = 32 * 5 * 2;
   const long P = kf->P;
   const size_t common = 2 * al(sizeof(float) * P) + al(P) + 256 +
                         al(sizeof(FusionArgs) * bands) + al(sizeof(void*) * bands);

@@ -26,7 +26,7 @@ struct BandLaunch {
   int nband, cpr, band0, sys;
 };
 
-__global__ void __launch_bounds__(FT, 1) k_fusion_banded(BandLaunch L) {
+__global__ void __launch_bounds__(FT, 2) k_fusion_banded(BandLaunch L) {  // as k_fusion<0, 0>
   __shared__ FusionArgs s_args;  // fields survive the L1 invalidation of every fence
   const int band = L.band0 + (int)(blockIdx.x / L.cpr);
   if (threadIdx.x == 0) s_args = L.args[band];
@@ -204,6 +204,7 @@ int fusion_grid(dfuse_ctx* ctx) {
 }
 
 size_t fusion_slots_bytes(int grid) {
+  grid *= 2;  // room for the streaming kernel's two CTAs per SM
   // LL slots (2 parities x 4 values x grid x 256 B) or the atomic-counter
   // microbenchmark variants' ReduceSlots, whichever is larger
   const size_t ll = sizeof(unsigned long long) * kSlotWords * 8 * (size_t)grid;
@@ -290,7 +291,12 @@ void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
     case 51: launch_fusion_t<5, 1>(ctx, a, grid); break;
     case 52: launch_fusion_t<5, 2>(ctx, a, grid); break;
     case 60: launch_fusion_t<6, 0>(ctx, a, grid); break;
-    default: launch_fusion_t<0, 0>(ctx, a, grid); break;
+    default: {  // streaming: two CTAs per SM (k_fusion<0, 0> launch bounds)
+      int g2 = 2 * grid;
+      if (g2 > 32 * kPollWarps * kMaxPollSlots) g2 = 32 * kPollWarps * kMaxPollSlots;
+      launch_fusion_t<0, 0>(ctx, a, g2);
+      break;
+    }
   }
   DF_LAUNCHED(ctx);
   if (ctx->trace) {  // diagnostics only (DFUSE_TRACE=1): per-phase cycles of the resident PCG
