@@ -293,9 +293,19 @@ def main():
     if ws > 1:
         import torch.distributed as dist
 
+        # one rank per GPU; with fewer GPUs than ranks (validating the
+        # multi-rank path of independent keyframe streams on one GPU) the
+        # ranks share devices -- they never wait on one another
+        shared = torch.cuda.device_count() < ws
+        local = local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:  # NCCL needs one device per rank
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = local
+    red_dev = (f"cuda:{device}" if ws > 1 and torch.distributed.get_backend() == "nccl"
+               else "cpu")  # device of the max-over-ranks reductions
     from paper_2207_12244_b200 import api
     from paper_2207_12244_b200._ffi import SemiDenseMap
 
@@ -398,7 +408,7 @@ def main():
     obs = [r.observations for r in stats_pass]
     total_ms = float(np.sum(step_ms))
     if ws > 1:
-        t = torch.tensor([total_ms], device=f"cuda:{device}", dtype=torch.float64)
+        t = torch.tensor([total_ms], device=red_dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     value = jobs * args.steps / (total_ms / 1e3)
@@ -424,7 +434,7 @@ def main():
             download(kf.handle, out_ld.ctypes.data, None, None, None, None, None, None, None)
         dt = time.perf_counter() - t0
         if ws > 1:
-            t = torch.tensor([dt], device=f"cuda:{device}", dtype=torch.float64)
+            t = torch.tensor([dt], device=red_dev, dtype=torch.float64)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             dt = float(t.item())
         e2e = {"value": round(jobs * args.steps / dt, 4), "unit": UNIT,
