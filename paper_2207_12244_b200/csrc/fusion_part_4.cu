@@ -1,4 +1,5 @@
 // fusion_part_4.cu -- k_fusion instantiations <4, 0>, <4, 1>, <4, 2> (see fusion_impl.cuh)
+#define DFUSE_RESIDENT_TU  // resident-PCG kernels: kResidentFT threads per CTA
 #include "fusion_launch.cuh"
 
 namespace dfuse_cuda {

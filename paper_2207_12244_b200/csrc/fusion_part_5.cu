@@ -1,4 +1,5 @@
 // fusion_part_5.cu -- k_fusion instantiations <5, 0>, <5, 1>, <5, 2> (see fusion_impl.cuh)
+#define DFUSE_RESIDENT_TU  // resident-PCG kernels: kResidentFT threads per CTA
 #include "fusion_launch.cuh"
 
 namespace dfuse_cuda {

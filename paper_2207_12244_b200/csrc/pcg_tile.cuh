@@ -719,5 +719,5 @@ __device__ int pcg_resident_2r(GridCtx& c, const FusionArgs& a, double bnorm2, d
 
 // shared memory of the resident PCG for a tw_max x th_max tile at ppt pixels per thread
 inline size_t pcg_tile_smem(int ppt, int tw_max, int th_max) {
-  return sizeof(double) * (8 * (size_t)ppt * FT + (size_t)(th_max + 2) * (tw_max + 2));
+  return sizeof(double) * (8 * (size_t)ppt * kResidentFT + (size_t)(th_max + 2) * (tw_max + 2));
 }
