@@ -215,7 +215,7 @@ size_t fusion_slots_bytes(int grid) {
 size_t fusion_halo_bytes(long P) { return sizeof(unsigned long long) * 6 * (size_t)P; }
 
 bool fusion_resident_possible(long P, int grid) {
-  return P <= (long)grid * 6 * kResidentFT;  // coarse bound; plan_tiles decides
+  return P <= (long)grid * DFUSE_PPT_HI * kResidentFT;  // coarse bound; plan_tiles decides
 }
 
 // tile partition for the resident PCG: tx x ty <= grid tiles, minimal
@@ -241,7 +241,7 @@ void plan_tiles(FusionArgs& a, int grid) {
   a.th_max = (a.H + by - 1) / by;
   const long T = (long)a.tw_max * a.th_max;
   constexpr long R = kResidentFT;
-  a.ppt = T <= 4 * R ? 4 : (T <= 5 * R ? 5 : (T <= 6 * R ? 6 : 0));
+  a.ppt = T <= 4 * R ? 4 : (T <= 5 * R ? 5 : (T <= DFUSE_PPT_HI * R ? DFUSE_PPT_HI : 0));
   if (a.ppt > 0 && pcg_tile_smem(a.ppt, a.tw_max, a.th_max) > kMaxDynSmem) a.ppt = 0;
   // LL flags are 32-bit: the whole launch must fit
   if ((double)a.gn * ((double)a.cg_max + 2.0) > 2.0e9) a.ppt = 0;
@@ -290,9 +290,9 @@ void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
     case 50: launch_fusion_t<5, 0>(ctx, a, grid); break;
     case 51: launch_fusion_t<5, 1>(ctx, a, grid); break;
     case 52: launch_fusion_t<5, 2>(ctx, a, grid); break;
-    case 60: launch_fusion_t<6, 0>(ctx, a, grid); break;
-    case 61: launch_fusion_t<6, 1>(ctx, a, grid); break;
-    case 62: launch_fusion_t<6, 2>(ctx, a, grid); break;
+    case DFUSE_PPT_HI * 10: launch_fusion_t<DFUSE_PPT_HI, 0>(ctx, a, grid); break;
+    case DFUSE_PPT_HI * 10 + 1: launch_fusion_t<DFUSE_PPT_HI, 1>(ctx, a, grid); break;
+    case DFUSE_PPT_HI * 10 + 2: launch_fusion_t<DFUSE_PPT_HI, 2>(ctx, a, grid); break;
     default: {  // streaming: two CTAs per SM (k_fusion<0, 0> launch bounds)
       int g2 = 2 * grid;
       if (g2 > 32 * kPollWarps * kMaxPollSlots) g2 = 32 * kPollWarps * kMaxPollSlots;
