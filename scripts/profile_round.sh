@@ -9,6 +9,10 @@ python bench.py --regime fixed > $O/${T}_bench_c2_fixed.json 2> $O/${T}_bench_c2
 python bench.py --config C5 > $O/${T}_bench_c5.json 2> $O/${T}_bench_c5.err
 python bench.py --config C1 > $O/${T}_bench_c1.json 2> $O/${T}_bench_c1.err
 python bench.py --impl reference --steps 3 --warmup 3 > $O/${T}_bench_ref.json 2> $O/${T}_bench_ref.err
+python bench.py --config C4 --regime fixed --steps 3 --warmup 3 --no-cpu-baseline \
+    > $O/${T}_bench_c4_fixed.json 2> $O/${T}_bench_c4_fixed.err
+python bench.py --config C4 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e \
+    > $O/${T}_bench_c4.json 2> $O/${T}_bench_c4.err
 # launch list (the command first ran clean without ncu above)
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $O/${T}_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline \
