@@ -136,7 +136,7 @@ struct PcgTile {
         const bool bd = lx == 0 || ly == 0 || lx == tg.tw - 1 || ly == tg.th - 1;
         lyb_[j] = ly | (bd ? (1 << 30) : 0);
         const double d = __ldcg(a.diag + g);
-        const double rd = 1.0 / d;
+        const double rd = rcp_nr(d);
         s_diag()[k] = d;
         s_rdiag()[k] = rd;
         s_right()[k] = gx + 1 < W ? __ldcg(a.right + g) : 0.0;
