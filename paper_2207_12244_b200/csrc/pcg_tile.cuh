@@ -334,15 +334,15 @@ __device__ __forceinline__ int pcg_cg_core(GridCtx& c, const FusionArgs& a, PcgT
       }
       prev = rn;
       if (!more) break;
-      beta = v[1] / rz;
+      beta = div_nr(v[1], rz);
       rz = v[1];
-      pq = v[2] - beta * rz / alpha;
+      pq = v[2] - div_nr(beta * rz, alpha);
     }
     if (!(pq > 0.0)) {  // fusion.hpp:342
       status = DFUSE_E_CG_DIVERGENCE;
       break;
     }
-    alpha = rz / pq;
+    alpha = div_nr(rz, pq);
     *its = it + 1;
     // p = z + beta p, q = H z + beta q (p = z at it 0, fusion.hpp:329-330,
     // 364); x += alpha p, r -= alpha q, z = r/diag (fusion.hpp:345-359)
@@ -519,14 +519,14 @@ __device__ int pcg_resident_pipe(GridCtx& c, const FusionArgs& a, double bnorm2,
       prev = rn;
       if (!more) break;
       gamma = v[0];
-      beta = gamma / gamma_prev;
-      pq = v[1] - beta * gamma / alpha;
+      beta = div_nr(gamma, gamma_prev);
+      pq = v[1] - div_nr(beta * gamma, alpha);
     }
     if (!(pq > 0.0)) {  // fusion.hpp:342
       status = DFUSE_E_CG_DIVERGENCE;
       break;
     }
-    alpha = gamma / pq;
+    alpha = div_nr(gamma, pq);
     gamma_prev = gamma;
     *its = it + 1;
     // z = n + beta z, s = w + beta s, p = u + beta p; x += alpha p,
@@ -659,7 +659,7 @@ __device__ int pcg_resident_2r(GridCtx& c, const FusionArgs& a, double bnorm2, d
         streak = 0;
       }
       prev = rn;
-      beta = v2[1] / rz;
+      beta = div_nr(v2[1], rz);
       rz = v2[1];
     }
     if (!more) break;
@@ -683,7 +683,7 @@ __device__ int pcg_resident_2r(GridCtx& c, const FusionArgs& a, double bnorm2, d
       status = DFUSE_E_CG_DIVERGENCE;
       break;
     }
-    const double alpha = rz / v1[0];
+    const double alpha = div_nr(rz, v1[0]);
     double rr = 0.0, rzn = 0.0;
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
