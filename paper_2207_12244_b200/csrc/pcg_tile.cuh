@@ -403,7 +403,8 @@ constexpr double kPipeSwitch = 1e-20;
 
 // Pipelined: one all-reduce per iteration, in flight during the halo
 // exchange and SpMV. Trace phases: 0 halo ring, 1 SpMV, 2 all-reduce wait,
-// 5 update sweep + publish.
+// 3 scalars + update sweep, 4 CTA reduction + publish,
+// 5 boundary words of m.
 //
 // The halo words of m alternate between two LL arrays by version parity: a
 // CTA posts m_{i+1} only after the all-reduce of iteration i, which needs
@@ -562,8 +563,10 @@ __device__ int pcg_resident_pipe(GridCtx& c, const FusionArgs& a, double bnorm2,
         rr += r * r;
       }
     }
+    trc.mark(3);  // (diagnostics: scalars + update sweep)
     double v2[3] = {ru, wu2, rr};
     grid_allreduce_publish(c, v2);  // its barrier follows every m write
+    trc.mark(4);  // (CTA reduction + publish)
     t.post_boundary(a, hm, base + (unsigned)it + 3u);
     trc.mark(5);
   }
