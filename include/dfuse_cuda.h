@@ -159,6 +159,13 @@ int dfuse_ctx_set_solver_ctas(dfuse_ctx* ctx, int ctas);
 int dfuse_ctx_set_solver_path(dfuse_ctx* ctx, int path);
 /* kernels launched on this context since creation (evidence counter) */
 int64_t dfuse_ctx_launch_count(const dfuse_ctx* ctx);
+/* the epipolar scan reads the tracked frame through a texture gather (one
+ * tld4 per bilinear sample, the same texels: bit-identical results) when the
+ * buffer meets the texture alignment; on = 0 forces plain loads (A/B, tests).
+ * Default on. */
+int dfuse_ctx_set_stereo_texture(dfuse_ctx* ctx, int on);
+/* scan launches that used the texture gather (evidence counter) */
+int64_t dfuse_ctx_texture_launches(const dfuse_ctx* ctx);
 /* diagnostics: device time (ms) of one cooperative launch running n grid-wide
  * all-reduces of the fusion solver on `grid` CTAs (variant 10 = production LL
  * all-to-all, 2 = atomic arrival counter) */

@@ -123,6 +123,21 @@ class Context:
     def launch_count(self) -> int:
         return int(lib().dfuse_ctx_launch_count(self.handle))
 
+    def set_stereo_texture(self, on: bool) -> None:
+        """Epipolar scan reads the tracked frame through a texture gather
+        (default) or plain loads; the results are bit-identical."""
+        L = lib()
+        L.dfuse_ctx_set_stereo_texture.argtypes = [C.c_void_p, C.c_int]
+        rc = L.dfuse_ctx_set_stereo_texture(self.handle, 1 if on else 0)
+        if rc:
+            raise DfuseError(rc, "dfuse_ctx_set_stereo_texture")
+
+    def texture_launches(self) -> int:
+        L = lib()
+        L.dfuse_ctx_texture_launches.argtypes = [C.c_void_p]
+        L.dfuse_ctx_texture_launches.restype = C.c_int64
+        return int(L.dfuse_ctx_texture_launches(self.handle))
+
     def close(self) -> None:
         if self.handle:
             lib().dfuse_ctx_destroy(self.handle)

@@ -290,6 +290,8 @@ int dfuse_ctx_destroy(dfuse_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& t : ctx->tex_cache)
+    if (t.tex) cudaDestroyTextureObject(t.tex);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   return DFUSE_OK;
@@ -304,6 +306,14 @@ int dfuse_ctx_set_solver_ctas(dfuse_ctx* ctx, int ctas) {
   ctx->solver_ctas = ctas;
   return DFUSE_OK;
 }
+
+int dfuse_ctx_set_stereo_texture(dfuse_ctx* ctx, int on) {
+  if (!ctx) return DFUSE_E_INVALID_ARGUMENT;
+  ctx->stereo_tex = on ? 1 : 0;
+  return DFUSE_OK;
+}
+
+int64_t dfuse_ctx_texture_launches(const dfuse_ctx* ctx) { return ctx ? ctx->tex_launches : 0; }
 
 int dfuse_debug_sync_bench(dfuse_ctx* ctx, int n, int variant, int grid, float* ms) {
   return guarded(ctx, [&] {

@@ -41,6 +41,16 @@ struct dfuse_ctx {
   dfuse_cuda::Buffer scratch[32];
   // pinned host staging for small results
   void* host_small = nullptr;
+  // texture objects over tracked frames (stereo.cu frame_texture)
+  struct TexEntry {
+    const void* ptr = nullptr;
+    int w = 0, h = 0;
+    unsigned long long tex = 0;
+  };
+  TexEntry tex_cache[16];
+  int tex_next = 0;
+  int stereo_tex = 1;         // dfuse_ctx_set_stereo_texture
+  int64_t tex_launches = 0;   // scan launches through the texture gather
 };
 
 namespace dfuse_cuda {

@@ -17,6 +17,7 @@ struct StereoArgs {
   dfuse_search_cfg cfg;
   const float* I0;
   const float* I1;
+  cudaTextureObject_t tex1;  // set by launch_stereo (frame_texture)
   int n_items;
   int* work_counter;
   // scan mode: masked-pixel list + semi map (in/out)

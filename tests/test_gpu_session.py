@@ -114,3 +114,30 @@ def test_session_c5_stress_matches_oracle(gpu_ctx, orc):
         assert rel_err(g_st.scale, o_st.scale) < 1e-4
         assert abs(res.stats.pcg_total - so.pcg_total) <= max(2, 0.02 * so.pcg_total)
     kf.close()
+
+
+@pytest.mark.parametrize("name", ["S", "C2"])
+def test_texture_gather_scan_is_bit_identical(orc, name):
+    """The epipolar scan through the texture gather (dfuse_ctx_set_stereo_texture,
+    default) and through plain loads give the same semi-dense map and fused
+    state, bit for bit; the session uses the gather."""
+    spec = synth.small_spec(160, 120, frames=3) if name == "S" else synth.CONFIGS["C2"]
+    seq = synth.make_sequence(spec, 5, frames=3)
+    cfg = RobustConfig(gn_iterations=spec.gn_iterations)
+    out = {}
+    for on in (True, False):
+        ctx = api.Context(0)
+        ctx.set_stereo_texture(on)
+        kf = api.Keyframe(ctx, spec.camera(), seq.I0, seq.pred, 0.02)
+        obs = []
+        for (q, t, I1) in seq.frames:
+            g = orc.make_epipolar_geometry(synth.IDENTITY_Q, np.zeros(3), q, t, spec.camera())
+            obs.append(kf.process_frame(g, I1, spec.search, cfg, "full").observations)
+        st, semi, _ = kf.download()
+        out[on] = (obs, st.log_depth.tobytes(), semi.depth.tobytes(), semi.variance.tobytes(),
+                   ctx.texture_launches())
+        kf.close()
+        ctx.close()
+    assert out[True][4] == len(seq.frames)  # the gather path ran
+    assert out[False][4] == 0
+    assert out[True][:4] == out[False][:4]
