@@ -459,6 +459,10 @@ __device__ int pcg_resident_pipe(GridCtx& c, const FusionArgs& a, double bnorm2,
 
   const double tol2 = a.cg_tol * a.cg_tol * bnorm2;
   double prev = bnorm2, alpha = 1.0, gamma_prev = rz;
+  // reciprocals of the previous iteration's scalars, formed before the
+  // all-reduce wait so that only 1/p.q stays on the path after it (the
+  // quotients are div_nr's, bit for bit)
+  double r_gp = rcp_nr(gamma_prev), r_al = 1.0;
   int streak = 0, status = 0;
   *its = 0;
   for (int it = 0;; ++it) {
@@ -520,8 +524,8 @@ __device__ int pcg_resident_pipe(GridCtx& c, const FusionArgs& a, double bnorm2,
       prev = rn;
       if (!more) break;
       gamma = v[0];
-      beta = div_nr(gamma, gamma_prev);
-      pq = v[1] - div_nr(beta * gamma, alpha);
+      beta = div_rb(gamma, gamma_prev, r_gp);
+      pq = v[1] - div_rb(beta * gamma, alpha, r_al);
     }
     if (!(pq > 0.0)) {  // fusion.hpp:342
       status = DFUSE_E_CG_DIVERGENCE;
@@ -529,6 +533,8 @@ __device__ int pcg_resident_pipe(GridCtx& c, const FusionArgs& a, double bnorm2,
     }
     alpha = div_nr(gamma, pq);
     gamma_prev = gamma;
+    r_gp = rcp_nr(gamma_prev);
+    r_al = rcp_nr(alpha);
     *its = it + 1;
     // z = n + beta z, s = w + beta s, p = u + beta p; x += alpha p,
     // r -= alpha s, w -= alpha z; u = r/diag, m = w/diag (fusion.hpp:345-364)
