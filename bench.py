@@ -13,9 +13,11 @@ step) and the sequence repeats.
   value   device-timed (CUDA events on the library's stream), input frames
           already resident in HBM, L2 flushed before every step (a 512 MiB
           write outside the timed events)
-  e2e     the same metric through the C-ABI with HOST buffers: H2D of the
-          tracked frame and D2H of the fused log-depth map inside the timed
-          region (wall clock around the synchronous calls)
+  e2e     the same metric through the C-ABI with HOST buffers
+          (dfuse_kf_process_frame_host_async): every step copies its tracked
+          frame in from pinned host memory and its fused log-depth map out to
+          pinned host memory (copy stream, overlapped with the neighbouring
+          frames' compute); wall clock from the first call to last_result()
   roofline  k_fusion (the dominant kernel): algorithmic bytes of the executed
           sweeps (SURVEY.md 8(d) byte model) / its device time, vs the measured
           HBM copy bandwidth in MEASURED_PEAKS.json
@@ -426,12 +428,29 @@ def main():
         out_ld = out_pinned.numpy()
         kf.reset()
         counter[0] = 0
+        # the pipelined host-buffer call where the keyframe has it: frame n's
+        # copy-in overlaps frame n-1's compute, its log-depth is copied out
+        # while frame n+1 computes (two pinned result slots, alternating)
+        host_async = hasattr(kf, "process_frame_host_async") and not isinstance(
+            kf, api.BandedKeyframe)
+        outs = [out_ld, torch.empty((spec.height, spec.width),
+                                    dtype=torch.float64).pin_memory().numpy()]
         if ws > 1:
             torch.distributed.barrier()
         t0 = time.perf_counter()
-        for _ in range(args.steps):
-            step(dev=False, host_images=host_imgs)
-            download(kf.handle, out_ld.ctypes.data, None, None, None, None, None, None, None)
+        if host_async:
+            for s_ in range(args.steps):
+                k = counter[0] % nF
+                if k == 0 and counter[0] > 0:
+                    kf.reset()
+                counter[0] += 1
+                kf.process_frame_host_async(geoms[k], host_imgs[k], spec.search, cfg, "full",
+                                            log_depth_out=outs[s_ & 1])
+            kf.last_result()
+        else:
+            for _ in range(args.steps):
+                step(dev=False, host_images=host_imgs)
+                download(kf.handle, out_ld.ctypes.data, None, None, None, None, None, None, None)
         dt = time.perf_counter() - t0
         if ws > 1:
             t = torch.tensor([dt], device=red_dev, dtype=torch.float64)

@@ -375,6 +375,17 @@ int dfuse_kf_process_frame_async(dfuse_keyframe* kf, const dfuse_epigeom* g,
                                  const float* I1_dev, const dfuse_search_cfg* scfg,
                                  const dfuse_robust_cfg* rcfg, int mode);
 int dfuse_kf_last_result(dfuse_keyframe* kf, dfuse_frame_result* res);
+/* The same for a HOST image, pipelined: the image is copied in on a copy
+ * stream while the previous frame computes, and, when log_depth_host is not
+ * null, the frame's fused log-depth (W*H doubles, what dfuse_kf_download
+ * returns after this frame) is copied out while the next frame computes.
+ * Both buffers should be pinned (cudaHostAlloc) for the copies to be
+ * asynchronous, and must stay untouched until dfuse_kf_last_result (which
+ * also waits for the copies). */
+int dfuse_kf_process_frame_host_async(dfuse_keyframe* kf, const dfuse_epigeom* g,
+                                      const float* I1_host, const dfuse_search_cfg* scfg,
+                                      const dfuse_robust_cfg* rcfg, int mode,
+                                      double* log_depth_host);
 /* copy state back to the host (any pointer may be NULL) */
 int dfuse_kf_download(dfuse_keyframe* kf, double* log_depth, double* scale, int32_t* iteration,
                       double* semi_depth, double* semi_variance, uint8_t* semi_valid,

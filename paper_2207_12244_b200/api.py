@@ -285,6 +285,32 @@ class Keyframe:
             self.handle, C.byref(g), C.c_void_p(device_ptr), C.byref(self._sc),
             C.byref(self._rc), _mode(mode)), "dfuse_kf_process_frame_async")
 
+    def process_frame_host_async(self, g: EpiGeom, I1_host: np.ndarray,
+                                 search: SearchConfig | None = None,
+                                 robust: RobustConfig | None = None, mode="full",
+                                 log_depth_out: np.ndarray | None = None) -> None:
+        """process_frame for a HOST image, pipelined
+        (dfuse_kf_process_frame_host_async): the copy-in overlaps the previous
+        frame's compute, and the fused log-depth lands in log_depth_out
+        (float64 [H, W]) while the next frame computes. Pass pinned arrays
+        (torch.empty(..).pin_memory().numpy()) and keep them untouched until
+        last_result()."""
+        search = search or SearchConfig()
+        robust = robust or RobustConfig()
+        self._sc, self._rc = search.c(), robust.c()
+        assert I1_host.dtype == np.float32 and I1_host.flags.c_contiguous
+        out = None
+        if log_depth_out is not None:
+            assert log_depth_out.dtype == np.float64 and log_depth_out.flags.c_contiguous
+            out = C.c_void_p(log_depth_out.ctypes.data)
+        L = lib()
+        L.dfuse_kf_process_frame_host_async.argtypes = [
+            C.c_void_p, C.POINTER(EpiGeom), C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+            C.c_void_p]
+        self._check(L.dfuse_kf_process_frame_host_async(
+            self.handle, C.byref(g), C.c_void_p(I1_host.ctypes.data), C.byref(self._sc),
+            C.byref(self._rc), _mode(mode), out), "dfuse_kf_process_frame_host_async")
+
     def last_result(self):
         res = FrameResultC()
         self._check(lib().dfuse_kf_last_result(self.handle, C.byref(res)), "dfuse_kf_last_result")

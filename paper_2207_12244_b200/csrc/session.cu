@@ -47,6 +47,18 @@ struct dfuse_keyframe {
   double median_depth = -1.0;      // cached median_predicted_depth (< 0: not computed)
   bool pending = false;            // a frame was enqueued and not yet collected
   FusionStateDev* h_s0 = nullptr;  // pinned: init_state's scalars for reset
+  // host-buffer pipeline (dfuse_kf_process_frame_host_async), made on first
+  // use: two frame slots and two result slots, a copy-in and a copy-out
+  // stream (so that frame n+1's copy-in never queues behind frame n's
+  // copy-out), and events ordering slot reuse between the streams
+  struct HostPipe {
+    float* img[2] = {};
+    double* out[2] = {};
+    cudaStream_t copy = nullptr, copy_out = nullptr;
+    cudaEvent_t in[2] = {}, read[2] = {}, staged[2] = {}, done[2] = {};
+    long n = 0;
+  } hp;
+  bool hp_used = false;
 };
 
 namespace {
@@ -95,6 +107,50 @@ void reset_state(dfuse_keyframe* kf) {
   kf->parity = 0;
   DF_CUDA(cudaMemcpyAsync(kf->st, kf->h_s0, sizeof(FusionStateDev), cudaMemcpyHostToDevice,
                           ctx->stream));
+}
+
+// the fused log-depth (ld[st->cur]) into a staging slot, on the device:
+// the host does not know cur without a synchronisation
+__global__ void k_copy_state_ld(const FusionStateDev* __restrict__ st,
+                                const double* __restrict__ ld0, const double* __restrict__ ld1,
+                                double* __restrict__ out, long P) {
+  const double* src = st->cur ? ld1 : ld0;
+  const long n2 = P / 2;  // 16-byte vectors (the buffers are 256-byte aligned), odd tail below
+  const double2* s2 = reinterpret_cast<const double2*>(src);
+  double2* o2 = reinterpret_cast<double2*>(out);
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n2;
+       i += (long)gridDim.x * blockDim.x)
+    o2[i] = s2[i];
+  if ((P & 1) && blockIdx.x == 0 && threadIdx.x == 0) out[P - 1] = src[P - 1];
+}
+
+void host_pipe_init(dfuse_keyframe* kf) {
+  auto& h = kf->hp;
+  if (h.copy) return;
+  const size_t P = (size_t)kf->P;
+  for (int b = 0; b < 2; ++b) {
+    DF_CUDA(cudaMalloc(&h.img[b], sizeof(float) * P));
+    DF_CUDA(cudaMalloc(&h.out[b], sizeof(double) * P));
+    for (cudaEvent_t* e : {&h.in[b], &h.read[b], &h.staged[b], &h.done[b]})
+      DF_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  DF_CUDA(cudaStreamCreateWithFlags(&h.copy, cudaStreamNonBlocking));
+  DF_CUDA(cudaStreamCreateWithFlags(&h.copy_out, cudaStreamNonBlocking));
+}
+
+void host_pipe_free(dfuse_keyframe* kf) {
+  auto& h = kf->hp;
+  if (!h.copy) return;
+  cudaStreamSynchronize(h.copy);
+  cudaStreamSynchronize(h.copy_out);
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(h.img[b]);
+    cudaFree(h.out[b]);
+    for (cudaEvent_t e : {h.in[b], h.read[b], h.staged[b], h.done[b]}) cudaEventDestroy(e);
+  }
+  cudaStreamDestroy(h.copy);
+  cudaStreamDestroy(h.copy_out);
+  h = dfuse_keyframe::HostPipe{};
 }
 
 // process_frame, enqueued on the context's stream (no host synchronisation):
@@ -163,6 +219,7 @@ void collect(dfuse_keyframe* kf, dfuse_frame_result* res) {
   DF_CUDA(cudaMemcpyAsync(kf->h_ctl, kf->fa.ctl, sizeof(FusionControl), cudaMemcpyDeviceToHost,
                           ctx->stream));
   DF_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (kf->hp.copy_out) DF_CUDA(cudaStreamSynchronize(kf->hp.copy_out));  // the results' copies
   kf->pending = false;
   if (kf->h_ctl->sync_phase > (1u << 30) || kf->h_ctl->sync_ll > (1u << 30))
     clear_sync(kf);  // 32-bit LL flags: start over long before they wrap
@@ -474,6 +531,7 @@ int dfuse_kf_destroy(dfuse_keyframe* kf) {
     cudaSetDevice(kf->ctx->device);
     cudaStreamSynchronize(kf->ctx->stream);
   }
+  host_pipe_free(kf);
   if (kf->block) cudaFree(kf->block);
   if (kf->h_ctl) cudaFreeHost(kf->h_ctl);
   if (kf->h_counters) cudaFreeHost(kf->h_counters);
@@ -515,6 +573,43 @@ int dfuse_kf_process_frame_async(dfuse_keyframe* kf, const dfuse_epigeom* g,
   return kf_guarded(kf, [&] {
     if (!I1_dev) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null image"};
     enqueue(kf, g, I1_dev, scfg, rcfg, mode);
+  });
+}
+
+// Host-buffer pipeline: frame n's H2D (copy stream) overlaps frame n-1's
+// compute; its fused log-depth is staged on the device after the solve and
+// copied out on the copy stream while frame n+1 computes.
+int dfuse_kf_process_frame_host_async(dfuse_keyframe* kf, const dfuse_epigeom* g,
+                                      const float* I1_host, const dfuse_search_cfg* scfg,
+                                      const dfuse_robust_cfg* rcfg, int mode,
+                                      double* log_depth_host) {
+  return kf_guarded(kf, [&] {
+    if (!I1_host) throw RefError{DFUSE_E_INVALID_ARGUMENT, "null image"};
+    dfuse_ctx* ctx = kf->ctx;
+    host_pipe_init(kf);
+    auto& h = kf->hp;
+    const int b = (int)(h.n & 1);
+    const size_t P = (size_t)kf->P;
+    // frame slot b: free once frame n-2 (its last reader) is done
+    DF_CUDA(cudaStreamWaitEvent(h.copy, h.read[b], 0));
+    DF_CUDA(cudaMemcpyAsync(h.img[b], I1_host, sizeof(float) * P, cudaMemcpyHostToDevice, h.copy));
+    DF_CUDA(cudaEventRecord(h.in[b], h.copy));
+    DF_CUDA(cudaStreamWaitEvent(ctx->stream, h.in[b], 0));
+    enqueue(kf, g, h.img[b], scfg, rcfg, mode);
+    DF_CUDA(cudaEventRecord(h.read[b], ctx->stream));
+    if (log_depth_host) {
+      // result slot b: free once frame n-2's copy-out is done
+      DF_CUDA(cudaStreamWaitEvent(ctx->stream, h.done[b], 0));
+      k_copy_state_ld<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(
+          kf->st + kf->parity, kf->fa.ld[0], kf->fa.ld[1], h.out[b], (long)P);
+      DF_LAUNCHED(ctx);
+      DF_CUDA(cudaEventRecord(h.staged[b], ctx->stream));
+      DF_CUDA(cudaStreamWaitEvent(h.copy_out, h.staged[b], 0));
+      DF_CUDA(cudaMemcpyAsync(log_depth_host, h.out[b], sizeof(double) * P,
+                              cudaMemcpyDeviceToHost, h.copy_out));
+      DF_CUDA(cudaEventRecord(h.done[b], h.copy_out));
+    }
+    h.n += 1;
   });
 }
 

@@ -141,3 +141,37 @@ def test_texture_gather_scan_is_bit_identical(orc, name):
     assert out[True][4] == len(seq.frames)  # the gather path ran
     assert out[False][4] == 0
     assert out[True][:4] == out[False][:4]
+
+
+def test_host_async_pipeline_equals_sync_frames(orc):
+    """dfuse_kf_process_frame_host_async: host frames copied in on the copy
+    stream, each frame's fused log-depth copied out while the next computes;
+    every frame's output equals the synchronous path's download, bit for bit."""
+    import torch
+
+    spec = synth.CONFIGS["C2"]
+    seq = synth.make_sequence(spec, 9, frames=5)
+    cfg = RobustConfig(gn_iterations=spec.gn_iterations)
+    ctx = api.Context(0)
+    kf = api.Keyframe(ctx, spec.camera(), seq.I0, seq.pred, 0.02)
+    geoms = [orc.make_epipolar_geometry(synth.IDENTITY_Q, np.zeros(3), q, t, spec.camera())
+             for (q, t, _) in seq.frames]
+    ref = []
+    for g, (_, _, I1) in zip(geoms, seq.frames):
+        last_sync = kf.process_frame(g, I1, spec.search, cfg, "full")
+        ref.append(kf.download()[0].log_depth.copy())
+    kf.reset()
+    pins = [torch.from_numpy(np.ascontiguousarray(I1, np.float32)).pin_memory()
+            for (_, _, I1) in seq.frames]
+    outs = [torch.empty((spec.height, spec.width), dtype=torch.float64).pin_memory()
+            for _ in seq.frames]
+    for g, p, o in zip(geoms, pins, outs):
+        kf.process_frame_host_async(g, p.numpy(), spec.search, cfg, "full",
+                                    log_depth_out=o.numpy())
+    res = kf.last_result()
+    for o, r in zip(outs, ref):
+        assert o.numpy().tobytes() == r.tobytes()
+    assert res.observations == last_sync.observations
+    assert res.stereo_frames == len(seq.frames)
+    kf.close()
+    ctx.close()
