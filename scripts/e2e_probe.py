@@ -48,5 +48,41 @@ def run(mode):
           flush=True)
 
 
+def run_events(flush_mb=0):
+    """device frames with events around each frame (as bench.py's timed
+    region; a fill of flush_mb MiB between frames, outside the events):
+    event sum vs wall clock"""
+    stream = torch.cuda.ExternalStream(ctx.stream_handle())
+    fl = torch.empty(max(1, flush_mb) * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    kf.reset()
+    torch.cuda.synchronize()
+    ev = []
+    t0 = time.perf_counter()
+    with torch.cuda.stream(stream):
+        for s in range(N):
+            k = s % nF
+            if k == 0 and s > 0:
+                kf.reset()
+            if flush_mb:
+                fl.fill_(float(s))
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            kf.process_frame_async(geoms[k], dev[k].data_ptr(), spec.search, cfg, "full")
+            e1.record(stream)
+            ev.append((e0, e1))
+    kf.last_result()
+    t2 = time.perf_counter()
+    inside = sum(a.elapsed_time(b) for a, b in ev)
+    span = ev[0][0].elapsed_time(ev[-1][1])
+    print(f"flush {flush_mb:4d} MiB events: inside {1e3 * inside / N:.1f} us/frame, first-to-last {1e3 * span / N:.1f} "
+          f"us/frame, wall {1e6 * (t2 - t0) / N:.1f} us/frame", flush=True)
+
+
+for mb in [0, 8, 64, 160, 512, 0]:
+    run_events(mb)
+samp = bench.ClockSampler(0)
+samp.start()
 for m in ["dev", "host", "host+out", "dev", "host+out"]:
     run(m)
+print("clocks", samp.stop())
