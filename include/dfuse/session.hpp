@@ -106,6 +106,29 @@ class DeviceKeyframe {
                          robust, mode);
   }
 
+  // Pipelined submission of a host frame (dfuse_kf_process_frame_host_async):
+  // returns at once; the frame is copied in while the previous one computes,
+  // and log_depth_out (width*height doubles, or null) receives this frame's
+  // fused log-depth while the next one computes. Use pinned buffers
+  // (cudaHostAlloc) for the copies to overlap; both must stay untouched until
+  // finish(), which waits and returns the last submitted frame's outcome.
+  void submit_frame(const EpipolarGeometry& g, const float* I1, const SearchConfig& search,
+                    const RobustConfig& robust, FusionMode mode, double* log_depth_out) {
+    const dfuse_epigeom cg = g.c_abi();
+    const dfuse_search_cfg sc = search.c_abi();
+    const dfuse_robust_cfg rc = robust.c_abi();
+    device::check(dfuse_kf_process_frame_host_async(kf_, &cg, I1, &sc, &rc,
+                                                    detail::mode_of(mode), log_depth_out),
+                  "submit_frame");
+  }
+
+  FrameOutcome finish() {
+    dfuse_frame_result r;
+    device::check(dfuse_kf_last_result(kf_, &r), "finish");
+    return {r.observations, r.inlier_count, r.stereo_frames, r.optimize_status, r.stereo_ms,
+            r.optimise_ms, r.stats};
+  }
+
   FusionState fusion() const {
     FusionState st{Raster<double>(K_.width, K_.height, 0.0), 1.0, 0};
     int32_t it = 0;

@@ -288,6 +288,27 @@ static void session_kats() {  // test_pipeline.cpp:57-73, 92-102
                                    robust, FusionMode::Full);
   CHECK(r2.observations == 0 && kf.fusion().iteration == 2 * robust.gn_iterations);
 
+  // the pipelined host-frame path gives the synchronous path's states
+  {
+    DeviceKeyframe ka(sc.K, I0, pred, 0.02), kb(sc.K, I0, pred, 0.02);
+    const IntensityImage f1 = sc.render({0.04, 0, 0}), f2 = sc.render({0.03, 0.01, 0});
+    const auto g1 = make_epipolar_geometry(Pose::identity(), translated(0.04), sc.K);
+    const auto g2 = make_epipolar_geometry(Pose::identity(), translated(0.03, 0.01), sc.K);
+    ka.process_frame(g1, f1, SearchConfig{1.0, 4.0}, robust, FusionMode::Full);
+    const FusionState s1 = ka.fusion();
+    const auto ra = ka.process_frame(g2, f2, SearchConfig{1.0, 4.0}, robust, FusionMode::Full);
+    const FusionState s2 = ka.fusion();
+    std::vector<double> o1(s1.log_depth.size()), o2(s1.log_depth.size());
+    kb.submit_frame(g1, f1.raster().data(), SearchConfig{1.0, 4.0}, robust, FusionMode::Full,
+                    o1.data());
+    kb.submit_frame(g2, f2.raster().data(), SearchConfig{1.0, 4.0}, robust, FusionMode::Full,
+                    o2.data());
+    const auto rb = kb.finish();
+    CHECK(rb.observations == ra.observations && rb.stereo_frames == 2);
+    CHECK(std::equal(o1.begin(), o1.end(), s1.log_depth.data()));
+    CHECK(std::equal(o2.begin(), o2.end(), s2.log_depth.data()));
+  }
+
   // make_keyframe from a DFPRED file (pipeline.hpp:133-147): written the way
   // save_predictions does (predictions.hpp:125-145), read back on the device
   const std::string path = "/tmp/dfuse_dropin_test.dfpred";
