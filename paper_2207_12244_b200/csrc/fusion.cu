@@ -221,19 +221,40 @@ bool fusion_resident_possible(long P, int grid) {
 // tile partition for the resident PCG: tx x ty <= grid tiles, minimal
 // largest tile, then minimal halo
 void plan_tiles(FusionArgs& a, int grid) {
-  long best = -1;
+  static const int force_tx = getenv("DFUSE_TILES_X") ? atoi(getenv("DFUSE_TILES_X")) : 0;
+  // Two cost models, measured: small tiles (<= 4 pixels per thread, latency
+  // bound: C1 320x240) take the smallest largest tile, then the smallest
+  // half perimeter (C1: 107x5 139 updates/s, 64x9 136). Large tiles take the
+  // largest tile's pixels plus 1.5 x its half perimeter (halo ring, boundary
+  // SpMV, boundary words), not narrower than 64 px, within the resident
+  // capacity. C2 (640x480, 148 CTAs), updates/s at the reference defaults by
+  // tiles_x: 3: 447, 4 (160x13): 466, 6: 473, 7 (92x23): 473, 9: 461,
+  // 10: 444, 12 (54x40): 450 -- the second model picks 7.
   int bx = 1, by = 1;
-  for (int tx = 1; tx <= grid && tx <= a.W; ++tx) {
-    int ty = grid / tx;
-    if (ty > a.H) ty = a.H;
-    if (ty < 1) break;
-    const long tw = (a.W + tx - 1) / tx, th = (a.H + ty - 1) / ty;
-    const long cost = tw * th * 64 + (tw + th);
-    if (best < 0 || cost < best) {
-      best = cost;
-      bx = tx;
-      by = ty;
+  for (int model = 0; model < 2; ++model) {
+    long best = -1;
+    for (int tx = 1; tx <= grid && tx <= a.W; ++tx) {
+      if (force_tx > 0 && tx != force_tx) continue;  // diagnostics: DFUSE_TILES_X
+      int ty = grid / tx;
+      if (ty > a.H) ty = a.H;
+      if (ty < 1) break;
+      const long tw = (a.W + tx - 1) / tx, th = (a.H + ty - 1) / ty;
+      long cost;
+      if (model == 0) {
+        cost = tw * th * 64 + (tw + th);
+      } else {
+        cost = 2 * tw * th + 3 * (tw + th);
+        if (tw < 64 && a.W >= 64) cost += 1L << 40;
+        if (tw * th > (long)DFUSE_PPT_HI * kResidentFT) cost += 1L << 41;
+      }
+      if (best < 0 || cost < best) {
+        best = cost;
+        bx = tx;
+        by = ty;
+      }
     }
+    const long T0 = (long)((a.W + bx - 1) / bx) * ((a.H + by - 1) / by);
+    if (model == 0 && T0 <= 4L * kResidentFT) break;  // small tiles: model 0 stands
   }
   a.tiles_x = bx;
   a.tiles_y = by;
