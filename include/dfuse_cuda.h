@@ -261,6 +261,9 @@ typedef struct {
   dfuse_solver_stats stats;
   int64_t epipolar_steps; /* steps of all epipolar searches of the frame
                              (semidense.hpp:323), for the stereo roofline */
+  int32_t solver_ppt;     /* PCG data path of the solve: pixels per thread of
+                             the SM-resident tiles, 0 = streaming from L2/HBM */
+  int32_t reserved;
 } dfuse_frame_result;
 
 /* make_keyframe (pipeline.hpp:125-153) minus prediction I/O: uploads I0 and

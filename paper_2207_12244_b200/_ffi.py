@@ -106,7 +106,8 @@ class FrameResultC(C.Structure):
     _fields_ = [("observations", C.c_int32), ("inlier_count", C.c_int32),
                 ("stereo_frames", C.c_int32), ("optimize_status", C.c_int32),
                 ("stereo_ms", C.c_float), ("optimise_ms", C.c_float),
-                ("stats", SolverStatsC), ("epipolar_steps", C.c_int64)]
+                ("stats", SolverStatsC), ("epipolar_steps", C.c_int64),
+                ("solver_ppt", C.c_int32), ("reserved", C.c_int32)]
 
 
 # --------------------------------------------------------------------------

@@ -205,6 +205,7 @@ class Keyframe:
         load_predictions + focal_adjust to camera.fx, on the device)."""
         L = lib()
         self.ctx = ctx
+        self._inflight = []  # host buffers of enqueued host-async frames
         self.W, self.H = camera.width, camera.height
         self._I0 = _f32(I0)
         kc = camera.c()
@@ -297,12 +298,23 @@ class Keyframe:
         last_result()."""
         search = search or SearchConfig()
         robust = robust or RobustConfig()
-        self._sc, self._rc = search.c(), robust.c()
-        assert I1_host.dtype == np.float32 and I1_host.flags.c_contiguous
+        P = self.W * self.H
+        if not (isinstance(I1_host, np.ndarray) and I1_host.dtype == np.float32
+                and I1_host.flags.c_contiguous and I1_host.size == P):
+            raise DfuseError(27, f"process_frame_host_async: I1_host must be a C-contiguous "
+                                 f"float32 array of {P} pixels")
         out = None
         if log_depth_out is not None:
-            assert log_depth_out.dtype == np.float64 and log_depth_out.flags.c_contiguous
+            if not (isinstance(log_depth_out, np.ndarray) and log_depth_out.dtype == np.float64
+                    and log_depth_out.flags.c_contiguous and log_depth_out.size == P
+                    and log_depth_out.flags.writeable):
+                raise DfuseError(27, f"process_frame_host_async: log_depth_out must be a "
+                                     f"writeable C-contiguous float64 array of {P} pixels")
             out = C.c_void_p(log_depth_out.ctypes.data)
+        self._sc, self._rc = search.c(), robust.c()
+        # the copies run asynchronously: keep both buffers alive until
+        # last_result() / reset() has waited for them
+        self._inflight.append((I1_host, log_depth_out))
         L = lib()
         L.dfuse_kf_process_frame_host_async.argtypes = [
             C.c_void_p, C.POINTER(EpiGeom), C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
@@ -314,6 +326,7 @@ class Keyframe:
     def last_result(self):
         res = FrameResultC()
         self._check(lib().dfuse_kf_last_result(self.handle, C.byref(res)), "dfuse_kf_last_result")
+        self._inflight = []
         return res
 
     def download(self):

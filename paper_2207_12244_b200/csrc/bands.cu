@@ -187,6 +187,13 @@ void alloc_band(dfuse_banded_keyframe* kf, Band& b) {
   b.owned = true;
   bind_band(kf, b, (char*)base, kf->cpr);
   DF_CUDA(cudaMemsetAsync(b.counters, 0, 256, kf->ctx->stream));
+  // LL words and the control block are cleared once, here, before any peer
+  // can know this allocation exists (its IPC handle is exported only after
+  // creation returns): launches then continue the flags (persist_sync)
+  DF_CUDA(cudaMemsetAsync(b.fa.slots, 0, fusion_slots_bytes(kf->cpr), kf->ctx->stream));
+  DF_CUDA(cudaMemsetAsync(b.rank_slots, 0, band_rank_slots_bytes(kf->nband), kf->ctx->stream));
+  DF_CUDA(cudaMemsetAsync(b.fa.ctl, 0, sizeof(FusionControl), kf->ctx->stream));
+  b.fa.persist_sync = 1;
 }
 
 // BandNb of band g: the halo planes of its neighbours (HaloPlane order)
@@ -292,10 +299,10 @@ void process_bkf(dfuse_banded_keyframe* kf, const dfuse_epigeom* g, const float*
     f.band_cta0 = (k - first) * kf->cpr;
     args[k] = f;
     ++nlocal;
-    // LL flags restart at 1 every launch (every rank clears its own arrays
-    // before the launch; peers post into them only from inside theirs)
-    DF_CUDA(cudaMemsetAsync(f.slots, 0, fusion_slots_bytes(kf->cpr), ctx->stream));
-    DF_CUDA(cudaMemsetAsync(b.rank_slots, 0, band_rank_slots_bytes(kf->nband), ctx->stream));
+    // no per-launch clearing of the LL arrays: the flags continue from the
+    // previous launch (ctl->sync_phase, identical in every band), and every
+    // slot is rewritten each time its phase parity comes round, so 32-bit
+    // flag wrap-around never meets a stale word of the same value
   }
   DF_CUDA(cudaMemcpyAsync(kf->d_args, args.data(), sizeof(FusionArgs) * kf->nband,
                           cudaMemcpyHostToDevice, ctx->stream));
@@ -330,6 +337,8 @@ void process_bkf(dfuse_banded_keyframe* kf, const dfuse_epigeom* g, const float*
   DF_CUDA(cudaEventElapsedTime(&res->optimise_ms, ctx->ev[1], ctx->ev[2]));
   res->stats = kf->h_ctl->stats;
   res->epipolar_steps = steps;
+  res->solver_ppt = 0;  // the row-band solve streams
+  res->reserved = 0;
 }
 
 }  // namespace

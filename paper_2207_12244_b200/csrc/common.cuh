@@ -51,6 +51,12 @@ struct dfuse_ctx {
   int tex_next = 0;
   int stereo_tex = 1;         // dfuse_ctx_set_stereo_texture
   int64_t tex_launches = 0;   // scan launches through the texture gather
+  // per-device launch facts, filled on first use (kernel attributes and
+  // occupancy are per device, so they live in the context, not in statics)
+  int stereo_occ = 0;             // resident k_stereo CTAs per SM
+  int fusion_occ = 0;             // resident k_fusion CTAs per SM
+  size_t tex_base_align = 0, tex_pitch_align = 0;
+  size_t fusion_smem_set[64] = {};  // dynamic smem attribute set per k_fusion instantiation
 };
 
 namespace dfuse_cuda {

@@ -36,7 +36,11 @@ __global__ void __launch_bounds__(FT, 2) k_fusion_banded(BandLaunch L) {  // as 
   c.slots = a.slots;
   c.G = (unsigned)L.cpr;
   c.base_tag = 0;
-  c.phase = 0;
+  // LL flags continue from the band's previous launch (persist_sync): the
+  // slots are never cleared between launches, so no rank has to touch an
+  // array a peer may already be posting into. Every band runs the same
+  // all-reduces, so every band's control block carries the same phase.
+  c.phase = a.persist_sync ? a.ctl->sync_phase : 0u;
   c.syncs = 0;
   c.ll_next = 1;
   c.me = blockIdx.x % L.cpr;
@@ -72,6 +76,7 @@ __global__ void __launch_bounds__(FT, 2) k_fusion_banded(BandLaunch L) {  // as 
   if (leader) {
     ctl->status = status;
     ctl->stats.grid_syncs = c.syncs;
+    if (a.persist_sync) ctl->sync_phase = c.phase;
   }
 }
 
@@ -187,8 +192,8 @@ static unsigned long long next_tag() {
 constexpr size_t kMaxDynSmem = 227 * 1024;  // also in fusion_launch.cuh
 
 int fusion_grid(dfuse_ctx* ctx) {
-  static int occ = -1;
-  if (occ < 0) {
+  int& occ = ctx->fusion_occ;
+  if (occ <= 0) {
     // every grid-synchronising kernel is __launch_bounds__(FT, 1); these two
     // stand for the k_fusion instantiations of the fusion_part_*.cu units
     int o[2] = {0, 0};

@@ -11,7 +11,7 @@ void launch_fusion_t(dfuse_ctx* ctx, FusionArgs& a, int grid) {
   size_t smem = 0;
   if (PPT > 0) {
     smem = pcg_tile_smem(PPT, a.tw_max, a.th_max);
-    static size_t configured = 0;
+    size_t& configured = ctx->fusion_smem_set[PPT * 4 + VAR];  // per context = per device
     if (smem > configured) {
       DF_CUDA(cudaFuncSetAttribute((const void*)k_fusion<PPT, VAR>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

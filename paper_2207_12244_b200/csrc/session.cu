@@ -233,6 +233,8 @@ void collect(dfuse_keyframe* kf, dfuse_frame_result* res) {
   DF_CUDA(cudaEventElapsedTime(&res->stereo_ms, ctx->ev[0], ctx->ev[1]));
   DF_CUDA(cudaEventElapsedTime(&res->optimise_ms, ctx->ev[1], ctx->ev[2]));
   res->stats = kf->h_ctl->stats;
+  res->solver_ppt = kf->fa.ppt;  // set by launch_fusion's tile planner
+  res->reserved = 0;
 }
 
 // the session's one device allocation (make_keyframe's Keyframe, the

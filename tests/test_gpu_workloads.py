@@ -1,0 +1,175 @@
+"""GPU parity on the workloads bench.py times (BASELINE configs C2, C3, C4).
+
+Each test runs the device-resident session free-running over the config's
+tracked frames -- the GPU state is never re-seeded from the oracle, so any
+drift compounds exactly as it does in the benchmark -- and compares every
+frame with the oracle pipeline (the plain-C restatement, pinned bit for bit
+to the reference build by test_oracle_pin.py; the 4K stereo stage uses the
+reference build itself, OpenMP, for speed), following pipeline.hpp:203-227
+with retirement disabled:
+
+  * semi-dense map (depth, variance, valid) and inlier count: bit-exact;
+  * observation count: equal;
+  * exp(log_depth) and scale: within 1e-4 relative (north_star tolerance);
+  * GN iteration counter: equal; PCG iterations per frame: within 2 %.
+"""
+import numpy as np
+import pytest
+
+from paper_2207_12244_b200 import api, synth
+from paper_2207_12244_b200._ffi import DfuseError, RobustConfig, SemiDenseMap, init_state
+from helpers import rel_err
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+def _geoms(orc, spec, seq):
+    return [orc.make_epipolar_geometry(synth.IDENTITY_Q, np.zeros(3), q, t, spec.camera())
+            for (q, t, _) in seq.frames]
+
+
+def oracle_pipeline(orc, spec, seq, cfg, geoms, stereo=None):
+    """process_frame's tracked-frame branch (pipeline.hpp:203-227) over the
+    frames: stereo_scan + update_semidense, then optimize (state unchanged on
+    CgDivergence). Yields (n_obs, semi, state, pcg_total, status) per frame."""
+    stereo = stereo or orc
+    mask = orc.texture_mask(seq.I0, 0.02)
+    semi = SemiDenseMap.empty(spec.width, spec.height)
+    st = init_state(seq.pred)
+    out = []
+    for g, (_, _, I1) in zip(geoms, seq.frames):
+        r = stereo.stereo_update(g, seq.I0, I1, mask, semi, spec.search, want_obs=False)
+        semi = r.semi
+        try:
+            st, so = orc.optimize(st, semi, seq.pred, cfg, with_stats=True)
+            pcg, status = so.pcg_total, 0
+        except DfuseError as e:
+            assert e.code == "CgDivergence", e
+            pcg, status = None, e.code_value
+        out.append((r.n_obs, semi.copy(), st.copy(), pcg, status))
+    return out
+
+
+def compare_frame(res, kf, o, pcg_tol=0.02):
+    n_obs, o_semi, o_st, o_pcg, o_status = o
+    g_st, g_semi, _ = kf.download()
+    assert res.observations == n_obs
+    assert res.inlier_count == o_semi.inlier_count == g_semi.inlier_count
+    assert g_semi.depth.tobytes() == o_semi.depth.tobytes()
+    assert g_semi.variance.tobytes() == o_semi.variance.tobytes()
+    assert g_semi.valid.tobytes() == o_semi.valid.tobytes()
+    assert res.optimize_status == o_status
+    assert g_st.iteration == o_st.iteration
+    assert rel_err(np.exp(g_st.log_depth), np.exp(o_st.log_depth)) < TOL
+    assert rel_err(g_st.scale, o_st.scale) < TOL
+    if o_pcg is not None:
+        assert abs(res.stats.pcg_total - o_pcg) <= max(1, pcg_tol * o_pcg), \
+            (res.stats.pcg_total, o_pcg)
+    return g_st, g_semi
+
+
+@pytest.mark.parametrize("regime", ["defaults", "fixed"])
+def test_c2_session_ten_frames_and_reset(gpu_ctx, orc, regime):
+    """The bench workload: C2, 10 tracked frames at the reference defaults and
+    at the fixed effort (10 GN x 5 PCG), then a reset and the first frame
+    again (bit-identical to its first run)."""
+    spec = synth.CONFIGS["C2"]
+    seq = synth.make_sequence(spec, 0)  # bench.py's keyframe 0
+    cfg = (RobustConfig(gn_iterations=10) if regime == "defaults"
+           else RobustConfig(gn_iterations=10, cg_tol=0.0, cg_max_iters=5))
+    geoms = _geoms(orc, spec, seq)
+    ref = oracle_pipeline(orc, spec, seq, cfg, geoms)
+    kf = api.Keyframe(gpu_ctx, spec.camera(), seq.I0, seq.pred, 0.02)
+    first = None
+    for k, (g, (_, _, I1)) in enumerate(zip(geoms, seq.frames)):
+        res = kf.process_frame(g, I1, spec.search, cfg, "full")
+        g_st, _ = compare_frame(res, kf, ref[k])
+        if regime == "fixed" and ref[k][3] is not None:
+            assert res.stats.pcg_total == ref[k][3] == 50
+        if k == 0:
+            first = g_st.log_depth.tobytes()
+    assert res.stereo_frames == len(seq.frames)
+    kf.reset()
+    res = kf.process_frame(geoms[0], seq.frames[0][2], spec.search, cfg, "full")
+    assert kf.download()[0].log_depth.tobytes() == first
+    assert res.stereo_frames == 1
+    kf.close()
+
+
+def test_c2_async_submission_equals_sync(gpu_ctx, orc):
+    """bench.py's timed path (frames enqueued back to back, reset inside the
+    stream) ends in the state of the synchronous pass, bit for bit."""
+    import torch
+
+    spec = synth.CONFIGS["C2"]
+    seq = synth.make_sequence(spec, 0)
+    cfg = RobustConfig(gn_iterations=10)
+    geoms = _geoms(orc, spec, seq)
+    dev = [torch.from_numpy(np.ascontiguousarray(I1, np.float32)).cuda()
+           for (_, _, I1) in seq.frames]
+    torch.cuda.synchronize()
+    a = api.Keyframe(gpu_ctx, spec.camera(), seq.I0, seq.pred, 0.02)
+    for k in range(len(geoms)):
+        a.process_frame(geoms[k], None, spec.search, cfg, "full", device_ptr=dev[k].data_ptr())
+    sa, ma, _ = a.download()
+    b = api.Keyframe(gpu_ctx, spec.camera(), seq.I0, seq.pred, 0.02)
+    for rep in range(2):  # the second pass starts from a stream-ordered reset
+        b.reset()
+        for k in range(len(geoms)):
+            b.process_frame_async(geoms[k], dev[k].data_ptr(), spec.search, cfg, "full")
+    rb = b.last_result()
+    sb, mb, _ = b.download()
+    assert sa.log_depth.tobytes() == sb.log_depth.tobytes()
+    assert (sa.scale, sa.iteration) == (sb.scale, sb.iteration)
+    assert ma.depth.tobytes() == mb.depth.tobytes() and ma.valid.tobytes() == mb.valid.tobytes()
+    assert rb.stereo_frames == len(geoms)
+    a.close()
+    b.close()
+
+
+@pytest.mark.parametrize("seed", [0, 5])
+def test_c3_box_scene_two_frames(gpu_ctx, orc, seed):
+    """C3: a 3-8 plane / box scene (bench.py --config C3 keyframe `seed`),
+    two tracked frames at the reference defaults."""
+    spec = synth.CONFIGS["C3"]
+    seq = synth.make_sequence(spec, seed, frames=2)
+    cfg = RobustConfig(gn_iterations=spec.gn_iterations)
+    geoms = _geoms(orc, spec, seq)
+    ref = oracle_pipeline(orc, spec, seq, cfg, geoms)
+    kf = api.Keyframe(gpu_ctx, spec.camera(), seq.I0, seq.pred, 0.02)
+    for k, (g, (_, _, I1)) in enumerate(zip(geoms, seq.frames)):
+        compare_frame(kf.process_frame(g, I1, spec.search, cfg, "full"), kf, ref[k])
+    kf.close()
+
+
+@pytest.fixture(scope="module")
+def c4_case(orc):
+    """C4 4K keyframe, one tracked frame, gn_iterations=2, cg_tol=0,
+    cg_max_iters=5 (the fixed-effort form of the 500-GN config)."""
+    import oracle
+
+    spec = synth.CONFIGS["C4"]
+    seq = synth.make_sequence(spec, 0, frames=1)
+    cfg = RobustConfig(gn_iterations=2, cg_tol=0.0, cg_max_iters=5)
+    geoms = _geoms(orc, spec, seq)
+    stereo = oracle.reference() if oracle.have_reference() else orc
+    return spec, seq, cfg, geoms, oracle_pipeline(orc, spec, seq, cfg, geoms, stereo)
+
+
+@pytest.mark.parametrize("bands", [0, 2, 4])
+def test_c4_4k_streaming_and_bands(gpu_ctx, c4_case, bands):
+    """C4 through the streaming keyframe (bands = 0) and through the row-band
+    keyframe with 2 and 4 bands (the multi-GPU layout on one GPU)."""
+    spec, seq, cfg, geoms, ref = c4_case
+    if bands:
+        kf = api.BandedKeyframe(gpu_ctx, spec.camera(), seq.I0, seq.pred, bands, 0.02)
+    else:
+        kf = api.Keyframe(gpu_ctx, spec.camera(), seq.I0, seq.pred, 0.02)
+    res = kf.process_frame(geoms[0], seq.frames[0][2], spec.search, cfg, "full")
+    if not bands:
+        assert res.solver_ppt == 0  # 8.3 Mpx does not fit on chip: streaming PCG
+    compare_frame(res, kf, ref[0])
+    assert res.stats.pcg_total == ref[0][3] == 10
+    kf.close()
