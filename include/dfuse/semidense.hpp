@@ -137,8 +137,9 @@ inline EpipolarStatus photometric_error_5pt(const EpipolarGeometry& g, const Int
                                             double d, std::array<double, 5>& e) {
   const dfuse_epigeom cg = g.c_abi();
   int32_t st = 0;
-  device::check(dfuse_photometric_error_5pt(device::ctx(), &cg, I0.raster().data(),
-                                            I1.raster().data(), x.x, x.y, d, e.data(), &st),
+  device::check(dfuse_photometric_error_5pt_gen(device::ctx(), &cg, I0.raster().data(),
+                                                I0.generation(), I1.raster().data(),
+                                                I1.generation(), x.x, x.y, d, e.data(), &st),
                 "photometric_error_5pt");
   return static_cast<EpipolarStatus>(st);
 }
@@ -189,9 +190,12 @@ inline std::vector<EpipolarResult> search_depth_batch(
   std::vector<EpipolarObservation> obs(n);
   const dfuse_epigeom cg = g.c_abi();
   const dfuse_search_cfg cc = cfg.c_abi();
-  device::check(dfuse_search_depth(device::ctx(), &cg, I0.raster().data(), I1.raster().data(), n,
-                                   px.data(), pr.data(), has.data(), &cc, st.data(),
-                                   reinterpret_cast<dfuse_obs*>(obs.data()), nullptr, nullptr),
+  // the images' device copies are shared by every call and thread while
+  // their generations are unchanged (one upload per image version)
+  device::check(dfuse_search_depth_gen(device::ctx(), &cg, I0.raster().data(), I0.generation(),
+                                       I1.raster().data(), I1.generation(), n, px.data(),
+                                       pr.data(), has.data(), &cc, st.data(),
+                                       reinterpret_cast<dfuse_obs*>(obs.data()), nullptr, nullptr),
                 "search_depth");
   std::vector<EpipolarResult> out(n);
   for (int k = 0; k < n; ++k) {

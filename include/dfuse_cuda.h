@@ -197,6 +197,37 @@ int dfuse_search_depth(dfuse_ctx* ctx, const dfuse_epigeom* g, const float* I0, 
                        const dfuse_search_cfg* cfg, int32_t* status, dfuse_obs* obs,
                        int32_t* best, int32_t* n_steps);
 
+/* search_depth for VERSIONED host images (semidense.hpp:277-379): the
+ * caller guarantees that the pixels at I0 (I1) do not change while gen0
+ * (gen1) does not (the drop-in dfuse::IntensityImage hands out a fresh,
+ * process-unique generation on construction, copy and every mutable
+ * access). Device copies live in one process-wide cache keyed by (device,
+ * host pointer, bytes, generation), shared by every context, so the
+ * reference's per-pixel stereo_scan loop (pipeline.hpp:167-178, OpenMP
+ * threads each with its own context) uploads each image once. gen = 0:
+ * uncached (uploaded by this call). Otherwise as dfuse_search_depth. */
+int dfuse_search_depth_gen(dfuse_ctx* ctx, const dfuse_epigeom* g, const float* I0, uint64_t gen0,
+                           const float* I1, uint64_t gen1, int n, const double* px,
+                           const double* prior, const uint8_t* has_prior,
+                           const dfuse_search_cfg* cfg, int32_t* status, dfuse_obs* obs,
+                           int32_t* best, int32_t* n_steps);
+/* photometric_error_5pt with versioned images (see dfuse_search_depth_gen) */
+int dfuse_photometric_error_5pt_gen(dfuse_ctx* ctx, const dfuse_epigeom* g, const float* I0,
+                                    uint64_t gen0, const float* I1, uint64_t gen1, double x,
+                                    double y, double d, double e[5], int32_t* status);
+/* process-wide number of host->device image uploads and their bytes (the
+ * evidence that versioned images are uploaded once) */
+int dfuse_image_uploads(int64_t* count, int64_t* bytes);
+/* stereo_scan(kf, frame, camera, cfg), pipeline.hpp:157-190: every masked
+ * pixel searched with the prior (depth, sqrt(variance)) of the map where
+ * valid; the OK observations in raster order into obs (capacity W*H),
+ * *n_obs of them. The map is read only. One scan launch per frame. Images
+ * versioned as in dfuse_search_depth_gen. */
+int dfuse_stereo_scan(dfuse_ctx* ctx, const dfuse_epigeom* g, const float* I0, uint64_t gen0,
+                      const float* I1, uint64_t gen1, const uint8_t* mask, const double* depth,
+                      const double* variance, const uint8_t* valid, const dfuse_search_cfg* cfg,
+                      dfuse_obs* obs, int32_t* n_obs);
+
 /* photometric_error_5pt(g, I0, I1, x, d, e), semidense.hpp:227-243: the five
  * stencil residuals at one depth hypothesis; *status = DFUSE_EPI_* */
 int dfuse_photometric_error_5pt(dfuse_ctx* ctx, const dfuse_epigeom* g, const float* I0,
@@ -337,6 +368,15 @@ int dfuse_bkf_create_rank(dfuse_ctx* ctx, const dfuse_intrinsics* K, const float
                           int rank, dfuse_banded_keyframe** out);
 int dfuse_bkf_peer_info(dfuse_banded_keyframe* kf, dfuse_band_peer* out);
 int dfuse_bkf_connect(dfuse_banded_keyframe* kf, const dfuse_band_peer* peers);
+/* diagnostics of the multi-process layout, no solve: _put writes base + i
+ * (i = global pixel index) for this rank's two boundary rows into the
+ * neighbours' halo rows of halo plane `plane` (0..7: ld0, ld1, x, z, down,
+ * p0, p1, 1/var_gy) with the solver's halo stores over the peer mappings;
+ * _get reads this rank's own halo rows (y0 - 1 and y1; W doubles each,
+ * skipped at the raster edge) */
+int dfuse_bkf_debug_halo_put(dfuse_banded_keyframe* kf, int plane, double base);
+int dfuse_bkf_debug_halo_get(dfuse_banded_keyframe* kf, int plane, double* above,
+                             double* below);
 
 /* ---- scoring (eval.hpp:34-68, 221-226; pipeline.hpp:232-247) --------- */
 typedef struct {

@@ -5,6 +5,9 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <atomic>
+#include <memory>
+#include <mutex>
 #include <new>
 #include <vector>
 
@@ -353,43 +356,9 @@ int dfuse_search_depth(dfuse_ctx* ctx, const dfuse_epigeom* g, const float* I0, 
                        int n, const double* px, const double* prior, const uint8_t* has_prior,
                        const dfuse_search_cfg* cfg, int32_t* status, dfuse_obs* obs, int32_t* best,
                        int32_t* n_steps) {
-  return guarded(ctx, [&] {
-    check_geom(g);
-    require(cfg && I0 && I1 && (n == 0 || (px && status && obs)), DFUSE_E_INVALID_ARGUMENT,
-            "null pointer");
-    if (n <= 0) return;
-    const long P = (long)g->K.width * g->K.height;
-    StereoArgs a;
-    memset(&a, 0, sizeof a);
-    a.g = *g;
-    a.cfg = *cfg;
-    a.I0 = (const float*)scratch(ctx, S_IMG0, sizeof(float) * P);
-    a.I1 = (const float*)scratch(ctx, S_IMG1, sizeof(float) * P);
-    h2d(ctx, (void*)a.I0, I0, sizeof(float) * P);
-    h2d(ctx, (void*)a.I1, I1, sizeof(float) * P);
-    a.n_items = n;
-    a.work_counter = (int*)scratch(ctx, S_COUNTERS, 64);
-    a.px = (const double*)scratch(ctx, S_PX, sizeof(double) * 2 * n);
-    h2d(ctx, (void*)a.px, px, sizeof(double) * 2 * n);
-    if (prior) {
-      a.prior = (const double*)scratch(ctx, S_PRIOR, sizeof(double) * 2 * n);
-      h2d(ctx, (void*)a.prior, prior, sizeof(double) * 2 * n);
-      if (has_prior) {
-        a.has_prior = (const uint8_t*)scratch(ctx, S_HASPRIOR, n);
-        h2d(ctx, (void*)a.has_prior, has_prior, n);
-      }
-    }
-    a.status = scratch(ctx, S_STATUS, sizeof(int32_t) * n);
-    a.obs = (dfuse_obs*)scratch(ctx, S_OBS, sizeof(dfuse_obs) * n);
-    a.best = (int32_t*)scratch(ctx, S_BEST, sizeof(int32_t) * n);
-    a.n_steps = (int32_t*)scratch(ctx, S_NSTEPS, sizeof(int32_t) * n);
-    launch_stereo(ctx, a, true);
-    d2h(ctx, status, a.status, sizeof(int32_t) * n);
-    d2h(ctx, obs, a.obs, sizeof(dfuse_obs) * n);
-    if (best) d2h(ctx, best, a.best, sizeof(int32_t) * n);
-    if (n_steps) d2h(ctx, n_steps, a.n_steps, sizeof(int32_t) * n);
-    sync(ctx);
-  });
+  // unversioned images: uploaded by this call
+  return dfuse_search_depth_gen(ctx, g, I0, 0, I1, 0, n, px, prior, has_prior, cfg, status, obs,
+                                best, n_steps);
 }
 
 int dfuse_photometric_error_5pt(dfuse_ctx* ctx, const dfuse_epigeom* g, const float* I0,
@@ -527,6 +496,224 @@ int dfuse_stereo_update(dfuse_ctx* ctx, const dfuse_epigeom* g, const float* I0,
     sync(ctx);
   });
 }
+
+// ---------------------------------------------------------------------------
+// versioned host images: process-wide device copies
+//
+// The reference's stereo_scan calls search_depth once per masked pixel from
+// an OpenMP loop (pipeline.hpp:167-178), each call with the same two
+// images. Per call, the drop-in passes the images' generation
+// (dfuse::IntensityImage::generation(), renewed by every mutable access), and
+// the device copy is looked up by (device, host pointer, bytes, generation)
+// in one cache shared by every context of the process: one upload per image
+// version however many threads and pixels use it. Entries are reference
+// counted, so evicting one never frees a buffer a queued search still reads.
+namespace {
+
+struct CachedImage {
+  int device;
+  const void* host;
+  size_t bytes;
+  uint64_t gen;
+  std::shared_ptr<void> dev;
+  uint64_t tick;
+};
+constexpr int kImageCachePerDevice = 8;
+std::mutex g_img_mu;
+std::vector<CachedImage>* g_img = new std::vector<CachedImage>();  // never destroyed (exit order)
+uint64_t g_img_tick = 0;
+std::atomic<long long> g_uploads{0}, g_upload_bytes{0};
+
+struct ImageRef {
+  const float* ptr;
+  std::shared_ptr<void> hold;  // keeps a cached copy alive for the call
+};
+
+ImageRef device_image(dfuse_ctx* ctx, int slot, const float* host, size_t bytes, uint64_t gen) {
+  if (gen == 0) {  // unversioned: a private upload for this call
+    float* d = (float*)scratch(ctx, slot, bytes);
+    h2d(ctx, d, host, bytes);
+    g_uploads += 1;
+    g_upload_bytes += (long long)bytes;
+    return {d, nullptr};
+  }
+  std::lock_guard<std::mutex> lk(g_img_mu);
+  const uint64_t tick = ++g_img_tick;
+  size_t lru = SIZE_MAX;
+  int n = 0;
+  for (size_t k = 0; k < g_img->size(); ++k) {
+    CachedImage& e = (*g_img)[k];
+    if (e.device != ctx->device) continue;
+    if (e.host == host && e.bytes == bytes && e.gen == gen) {
+      e.tick = tick;
+      return {(const float*)e.dev.get(), e.dev};
+    }
+    ++n;
+    if (lru == SIZE_MAX || e.tick < (*g_img)[lru].tick) lru = k;
+  }
+  if (n >= kImageCachePerDevice) g_img->erase(g_img->begin() + (long)lru);
+  void* d = nullptr;
+  DF_CUDA(cudaMalloc(&d, bytes));
+  const int dev = ctx->device;
+  std::shared_ptr<void> hold(d, [dev](void* p) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(dev);
+    cudaFree(p);
+    cudaSetDevice(cur);
+  });
+  // complete before the entry is visible to any other context's stream
+  DF_CUDA(cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  DF_CUDA(cudaStreamSynchronize(ctx->stream));
+  g_uploads += 1;
+  g_upload_bytes += (long long)bytes;
+  g_img->push_back(CachedImage{dev, host, bytes, gen, hold, tick});
+  return {(const float*)d, hold};
+}
+
+// search_depth over a list of pixels on device images (dfuse_search_depth*)
+void search_list(dfuse_ctx* ctx, const dfuse_epigeom* g, const float* dI0, const float* dI1, int n,
+                 const double* px, const double* prior, const uint8_t* has_prior,
+                 const dfuse_search_cfg* cfg, int32_t* status, dfuse_obs* obs, int32_t* best,
+                 int32_t* n_steps) {
+  StereoArgs a;
+  memset(&a, 0, sizeof a);
+  a.g = *g;
+  a.cfg = *cfg;
+  a.I0 = dI0;
+  a.I1 = dI1;
+  a.n_items = n;
+  a.work_counter = (int*)scratch(ctx, S_COUNTERS, 64);
+  a.px = (const double*)scratch(ctx, S_PX, sizeof(double) * 2 * n);
+  h2d(ctx, (void*)a.px, px, sizeof(double) * 2 * n);
+  if (prior) {
+    a.prior = (const double*)scratch(ctx, S_PRIOR, sizeof(double) * 2 * n);
+    h2d(ctx, (void*)a.prior, prior, sizeof(double) * 2 * n);
+    if (has_prior) {
+      a.has_prior = (const uint8_t*)scratch(ctx, S_HASPRIOR, n);
+      h2d(ctx, (void*)a.has_prior, has_prior, n);
+    }
+  }
+  a.status = scratch(ctx, S_STATUS, sizeof(int32_t) * n);
+  a.obs = (dfuse_obs*)scratch(ctx, S_OBS, sizeof(dfuse_obs) * n);
+  a.best = (int32_t*)scratch(ctx, S_BEST, sizeof(int32_t) * n);
+  a.n_steps = (int32_t*)scratch(ctx, S_NSTEPS, sizeof(int32_t) * n);
+  launch_stereo(ctx, a, true);
+  d2h(ctx, status, a.status, sizeof(int32_t) * n);
+  d2h(ctx, obs, a.obs, sizeof(dfuse_obs) * n);
+  if (best) d2h(ctx, best, a.best, sizeof(int32_t) * n);
+  if (n_steps) d2h(ctx, n_steps, a.n_steps, sizeof(int32_t) * n);
+  sync(ctx);
+}
+
+}  // namespace
+
+extern "C" {
+
+int dfuse_image_uploads(int64_t* count, int64_t* bytes) {
+  if (count) *count = g_uploads.load();
+  if (bytes) *bytes = g_upload_bytes.load();
+  return DFUSE_OK;
+}
+
+int dfuse_search_depth_gen(dfuse_ctx* ctx, const dfuse_epigeom* g, const float* I0, uint64_t gen0,
+                           const float* I1, uint64_t gen1, int n, const double* px,
+                           const double* prior, const uint8_t* has_prior,
+                           const dfuse_search_cfg* cfg, int32_t* status, dfuse_obs* obs,
+                           int32_t* best, int32_t* n_steps) {
+  return guarded(ctx, [&] {
+    check_geom(g);
+    require(cfg && I0 && I1 && (n == 0 || (px && status && obs)), DFUSE_E_INVALID_ARGUMENT,
+            "null pointer");
+    if (n <= 0) return;
+    const size_t bytes = sizeof(float) * (size_t)g->K.width * g->K.height;
+    const ImageRef i0 = device_image(ctx, S_IMG0, I0, bytes, gen0);
+    const ImageRef i1 = device_image(ctx, S_IMG1, I1, bytes, gen1);
+    search_list(ctx, g, i0.ptr, i1.ptr, n, px, prior, has_prior, cfg, status, obs, best, n_steps);
+  });
+}
+
+int dfuse_photometric_error_5pt_gen(dfuse_ctx* ctx, const dfuse_epigeom* g, const float* I0,
+                                    uint64_t gen0, const float* I1, uint64_t gen1, double x,
+                                    double y, double d, double e[5], int32_t* status) {
+  return guarded(ctx, [&] {
+    check_geom(g);
+    require(I0 && I1 && e && status, DFUSE_E_INVALID_ARGUMENT, "null pointer");
+    const size_t bytes = sizeof(float) * (size_t)g->K.width * g->K.height;
+    const ImageRef i0 = device_image(ctx, S_IMG0, I0, bytes, gen0);
+    const ImageRef i1 = device_image(ctx, S_IMG1, I1, bytes, gen1);
+    double* out = (double*)scratch(ctx, S_TMP3, 8 * sizeof(double));
+    launch_photometric(ctx, *g, i0.ptr, i1.ptr, x, y, d, out);
+    double h[6];
+    d2h(ctx, h, out, sizeof h);
+    sync(ctx);
+    for (int j = 0; j < 5; ++j) e[j] = h[j];
+    *status = (int32_t)h[5];
+  });
+}
+
+// stereo_scan (pipeline.hpp:157-190): every masked pixel searched with the
+// prior read from the map; the OK observations in raster order. The map is
+// not changed: the kernel's fused update runs on a scratch copy (each pixel
+// reads only its own prior, so the observations are those of a read-only
+// scan) and is dropped.
+int dfuse_stereo_scan(dfuse_ctx* ctx, const dfuse_epigeom* g, const float* I0, uint64_t gen0,
+                      const float* I1, uint64_t gen1, const uint8_t* mask, const double* depth,
+                      const double* variance, const uint8_t* valid, const dfuse_search_cfg* cfg,
+                      dfuse_obs* obs, int32_t* n_obs) {
+  return guarded(ctx, [&] {
+    check_geom(g);
+    require(cfg && I0 && I1 && mask && depth && variance && valid && obs && n_obs,
+            DFUSE_E_INVALID_ARGUMENT, "null pointer");
+    const long P = (long)g->K.width * g->K.height;
+    const ImageRef i0 = device_image(ctx, S_IMG0, I0, sizeof(float) * P, gen0);
+    const ImageRef i1 = device_image(ctx, S_IMG1, I1, sizeof(float) * P, gen1);
+    StereoArgs a;
+    memset(&a, 0, sizeof a);
+    a.g = *g;
+    a.cfg = *cfg;
+    a.I0 = i0.ptr;
+    a.I1 = i1.ptr;
+    uint8_t* dmask = (uint8_t*)scratch(ctx, S_MASK, P);
+    h2d(ctx, dmask, mask, P);
+    a.depth = (double*)scratch(ctx, S_SEMI_D, sizeof(double) * P);
+    a.variance = (double*)scratch(ctx, S_SEMI_V, sizeof(double) * P);
+    a.valid = (uint8_t*)scratch(ctx, S_SEMI_VALID, P);
+    h2d(ctx, a.depth, depth, sizeof(double) * P);
+    h2d(ctx, a.variance, variance, sizeof(double) * P);
+    h2d(ctx, a.valid, valid, P);
+    int* counters = (int*)scratch(ctx, S_COUNTERS, 64);
+    DF_CUDA(cudaMemsetAsync(counters, 0, 64, ctx->stream));
+    int* list = (int*)scratch(ctx, S_LIST, sizeof(int) * P);
+    launch_mask_list(ctx, dmask, P, list, counters + 1);
+    int n_list = 0;
+    d2h(ctx, &n_list, counters + 1, sizeof(int));
+    sync(ctx);
+    a.list = list;
+    a.n_items = n_list;
+    a.work_counter = counters;
+    a.n_obs = counters + 2;
+    a.n_installed = counters + 3;
+    dfuse_obs* dense = (dfuse_obs*)scratch(ctx, S_OBS, sizeof(dfuse_obs) * P);
+    a.obs = dense;
+    a.obs_flag = (uint8_t*)scratch(ctx, S_TMP0, P);
+    DF_CUDA(cudaMemsetAsync(a.obs_flag, 0, P, ctx->stream));
+    if (n_list > 0) launch_stereo(ctx, a, false);
+    int nb = 0;
+    d2h(ctx, &nb, counters + 2, sizeof(int));
+    sync(ctx);
+    *n_obs = nb;
+    if (nb > 0) {
+      dfuse_obs* compact = (dfuse_obs*)scratch(ctx, S_TMP2, sizeof(dfuse_obs) * nb);
+      int* blocks = (int*)scratch(ctx, S_TMP1, sizeof(int) * ((P + 1023) / 1024 + 1));
+      launch_compact_obs(ctx, a.obs_flag, dense, P, blocks, compact);
+      d2h(ctx, obs, compact, sizeof(dfuse_obs) * nb);
+      sync(ctx);
+    }
+  });
+}
+
+}  // extern "C"
 
 // ---------------------------------------------------------------------------
 // fusion

@@ -341,6 +341,34 @@ void process_bkf(dfuse_banded_keyframe* kf, const dfuse_epigeom* g, const float*
   res->reserved = 0;
 }
 
+// the HaloPlane `plane` of a band's FusionArgs (the order of neighbours())
+double* halo_plane(const FusionArgs& f, int plane) {
+  switch (plane) {
+    case HP_LD0: return f.ld[0];
+    case HP_LD1: return f.ld[1];
+    case HP_X: return f.x;
+    case HP_Z: return f.z;
+    case HP_DOWN: return f.down;
+    case HP_P0: return f.p[0];
+    case HP_P1: return f.p[1];
+    case HP_IV2: return f.ivar[2];
+    default: throw RefError{DFUSE_E_INVALID_ARGUMENT, "unknown halo plane"};
+  }
+}
+
+// diagnostics: this band's boundary rows into the neighbours' halo rows with
+// the solver's halo_put stores (fusion_impl.cuh) -- remote stores when the
+// neighbour is a peer mapping -- value base + global pixel index
+__global__ void k_band_halo_probe(const BandNb* __restrict__ nb, int W, int y0, int y1, int plane,
+                                  double base) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < W; x += gridDim.x * blockDim.x) {
+    const long top = (long)y0 * W + x, bot = (long)(y1 - 1) * W + x;
+    if (nb->up[plane]) nb->up[plane][top] = base + (double)top;
+    if (nb->dn[plane]) nb->dn[plane][bot] = base + (double)bot;
+  }
+  __threadfence_system();
+}
+
 }  // namespace
 
 namespace {
@@ -528,6 +556,39 @@ int dfuse_bkf_connect(dfuse_banded_keyframe* kf, const dfuse_band_peer* peers) {
       bind_band(kf, b, (char*)base, pi.cpr);
     }
     bind_neighbours(kf);
+  });
+}
+
+int dfuse_bkf_debug_halo_put(dfuse_banded_keyframe* kf, int plane, double base) {
+  return bkf_guarded(kf, [&] {
+    if (!kf->connected) throw RefError{DFUSE_E_INVALID_ARGUMENT, "bands not connected"};
+    if (plane < 0 || plane >= HP_COUNT) throw RefError{DFUSE_E_INVALID_ARGUMENT, "bad plane"};
+    dfuse_ctx* ctx = kf->ctx;
+    for (Band& b : kf->bands) {
+      if (!b.local) continue;
+      k_band_halo_probe<<<(kf->W + 255) / 256, 256, 0, ctx->stream>>>(b.nb_dev, kf->W, b.y0,
+                                                                       b.y1, plane, base);
+      DF_LAUNCHED(ctx);
+    }
+    DF_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int dfuse_bkf_debug_halo_get(dfuse_banded_keyframe* kf, int plane, double* above,
+                             double* below) {
+  return bkf_guarded(kf, [&] {
+    if (kf->rank < 0) throw RefError{DFUSE_E_INVALID_ARGUMENT, "not a rank keyframe"};
+    const Band& b = kf->bands[kf->rank];
+    const double* p = halo_plane(b.fa, plane);
+    dfuse_ctx* ctx = kf->ctx;
+    const size_t row = sizeof(double) * kf->W;
+    if (above && b.y0 > 0)
+      DF_CUDA(cudaMemcpyAsync(above, p + (long)(b.y0 - 1) * kf->W, row, cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    if (below && b.y1 < kf->H)
+      DF_CUDA(cudaMemcpyAsync(below, p + (long)b.y1 * kf->W, row, cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    DF_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 

@@ -25,7 +25,8 @@ def test_header_declares_the_path():
               "dfuse_stereo_update", "dfuse_assemble_normal_equations", "dfuse_total_cost",
               "dfuse_cost_gradient", "dfuse_stencil_apply", "dfuse_solve_depth_step",
               "dfuse_solve_scale_step", "dfuse_optimize", "dfuse_kf_create",
-              "dfuse_kf_process_frame", "dfuse_make_epipolar_geometry"):
+              "dfuse_kf_process_frame", "dfuse_make_epipolar_geometry", "dfuse_stereo_scan",
+              "dfuse_search_depth_gen", "dfuse_bkf_connect"):
         assert n in names
 
 
