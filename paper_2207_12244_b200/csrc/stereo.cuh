@@ -5,11 +5,12 @@
 
 namespace dfuse_cuda {
 
+// the scalar outcome of one search; the observation itself is written to
+// the warp's shared slot (stereo.cu, Stencil::obs)
 struct SearchResult {
   int status;
   int best;
   int n_steps;
-  dfuse_obs obs;
 };
 
 struct StereoArgs {
