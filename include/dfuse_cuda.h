@@ -166,6 +166,11 @@ int64_t dfuse_ctx_launch_count(const dfuse_ctx* ctx);
 int dfuse_ctx_set_stereo_texture(dfuse_ctx* ctx, int on);
 /* scan launches that used the texture gather (evidence counter) */
 int64_t dfuse_ctx_texture_launches(const dfuse_ctx* ctx);
+/* keyframes created on this context keep prediction planes 1..5 as float32
+ * when every value is float-exact (the reference's own precision,
+ * predictions.hpp:16-17): half the prediction bytes per sweep, bit-identical
+ * results. on = 0 keeps fp64 planes (A/B, tests). Default on. */
+int dfuse_ctx_set_fp32_predictions(dfuse_ctx* ctx, int on);
 /* diagnostics: device time (ms) of one cooperative launch running n grid-wide
  * all-reduces of the fusion solver on `grid` CTAs (variant 10 = production LL
  * all-to-all, 2 = atomic arrival counter) */

@@ -318,6 +318,12 @@ int dfuse_ctx_set_stereo_texture(dfuse_ctx* ctx, int on) {
 
 int64_t dfuse_ctx_texture_launches(const dfuse_ctx* ctx) { return ctx ? ctx->tex_launches : 0; }
 
+int dfuse_ctx_set_fp32_predictions(dfuse_ctx* ctx, int on) {
+  if (!ctx) return DFUSE_E_INVALID_ARGUMENT;
+  ctx->pred_fp32 = on ? 1 : 0;
+  return DFUSE_OK;
+}
+
 int dfuse_debug_sync_bench(dfuse_ctx* ctx, int n, int variant, int grid, float* ms) {
   return guarded(ctx, [&] {
     require(ms != nullptr && n >= 0, DFUSE_E_INVALID_ARGUMENT, "bad arguments");

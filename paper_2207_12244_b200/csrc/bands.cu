@@ -104,7 +104,7 @@ inline int hi_row(const Band& b, int H) { return b.y1 < H ? b.y1 + 1 : H; }
 // per band, band count), so a peer can rebuild every pointer of a band it
 // maps by IPC from the base address alone.
 struct BandLayout {
-  size_t plane[BP_COUNT], valid, list, counters, slots, rank_slots, ctl, st, nb, total;
+  size_t plane[BP_COUNT], planef[5], valid, list, counters, slots, rank_slots, ctl, st, nb, total;
 };
 
 BandLayout band_layout(int W, int y0, int y1, int cpr, int nband) {
@@ -117,6 +117,7 @@ BandLayout band_layout(int W, int y0, int y1, int cpr, int nband) {
     return r;
   };
   for (int k = 0; k < BP_COUNT; ++k) L.plane[k] = take(sizeof(double) * n);
+  for (int k = 0; k < 5; ++k) L.planef[k] = take(sizeof(float) * n);  // predf[1..5]
   L.valid = take(n);
   L.list = take(sizeof(int) * (size_t)(y1 - y0) * W);
   L.counters = take(256);
@@ -148,6 +149,7 @@ void bind_band(dfuse_banded_keyframe* kf, Band& b, char* base, int cpr) {
   f.W = kf->W;
   f.H = kf->H;
   for (int c = 0; c < 6; ++c) f.pred[c] = sh[BP_PRED0 + c];
+  for (int c = 1; c < 6; ++c) f.predf[c] = (float*)(base + L.planef[c - 1]) - shift;
   b.semi_d = sh[BP_SD];
   b.semi_v = sh[BP_SV];
   f.sd = b.semi_d;
@@ -415,7 +417,7 @@ void create_bkf(dfuse_banded_keyframe* kf, const dfuse_intrinsics* K, const floa
   kf->cpr = 2 * fusion_grid(ctx) / per_process;
   if (kf->cpr > 32 * 5 * 2) kf->cpr = 32 * 5 * 2;
   const long P = kf->P;
-  const size_t common = 2 * al(sizeof(float) * P) + al(P) + 256 +
+  const size_t common = 2 * al(sizeof(float) * P) + al(P) + al(sizeof(int) * bands + 256) +
                         al(sizeof(FusionArgs) * bands) + al(sizeof(void*) * bands);
   DF_CUDA(cudaMalloc(&kf->common, common));
   char* p = (char*)kf->common;
@@ -427,7 +429,7 @@ void create_bkf(dfuse_banded_keyframe* kf, const dfuse_intrinsics* K, const floa
   kf->I0 = (float*)take(sizeof(float) * P);
   kf->I1 = (float*)take(sizeof(float) * P);
   kf->mask = (uint8_t*)take(P);
-  kf->shared = (int*)take(256);
+  kf->shared = (int*)take(sizeof(int) * bands + 256);  // per-band scratch counters
   kf->d_args = (FusionArgs*)take(sizeof(FusionArgs) * bands);
   kf->d_rank = (unsigned long long**)take(sizeof(void*) * bands);
   DF_CUDA(cudaMallocHost(&kf->h_ctl, sizeof(FusionControl)));
@@ -449,6 +451,33 @@ void create_bkf(dfuse_banded_keyframe* kf, const dfuse_intrinsics* K, const floa
                               sizeof(double) * (size_t)(r1 - r0) * kf->W, cudaMemcpyHostToDevice,
                               ctx->stream));
   }
+  // prediction planes 1..5 as float32 where every value (halo rows
+  // included) is float-exact; a band that is not keeps its fp64 planes
+  // (both forms give the same bits, so the bands may differ)
+  int* inexact = (int*)kf->shared;
+  DF_CUDA(cudaMemsetAsync(inexact, 0, sizeof(int) * bands, ctx->stream));
+  for (int g = 0; g < bands; ++g) {
+    Band& b = kf->bands[g];
+    if (!b.local) continue;
+    const long o = (long)lo_row(b) * kf->W;
+    const double* p64[6];
+    float* p32[6];
+    for (int c = 0; c < 6; ++c) {
+      p64[c] = b.fa.pred[c] + o;
+      p32[c] = c ? const_cast<float*>(b.fa.predf[c]) + o : nullptr;
+    }
+    launch_pred_narrow(ctx, p64, p32, (long)(hi_row(b, kf->H) - lo_row(b)) * kf->W, inexact + g);
+  }
+  std::vector<int> h_inexact(bands, 0);
+  DF_CUDA(cudaMemcpyAsync(h_inexact.data(), inexact, sizeof(int) * bands, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  DF_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int g = 0; g < bands; ++g)
+    if (kf->bands[g].local) {
+      Band& b = kf->bands[g];
+      b.fa.pred_f32_ok = (h_inexact[g] == 0 && ctx->pred_fp32);
+      b.fa.pred_f32 = b.fa.pred_f32_ok ? 1 : 0;  // the row-band solve streams: mode 1
+    }
   DF_CUDA(cudaMemcpyAsync(kf->I0, I0, sizeof(float) * P, cudaMemcpyHostToDevice, ctx->stream));
   // make_keyframe: texture_mask (pipeline.hpp:148), then each band's list
   launch_texture_mask(ctx, kf->I0, kf->W, kf->H, texture_threshold, kf->mask);

@@ -57,6 +57,7 @@ struct dfuse_ctx {
   int fusion_occ = 0;             // resident k_fusion CTAs per SM
   size_t tex_base_align = 0, tex_pitch_align = 0;
   size_t fusion_smem_set[64] = {};  // dynamic smem attribute set per k_fusion instantiation
+  int pred_fp32 = 1;  // sessions keep float-exact prediction planes as fp32 (dfuse_ctx_set_fp32_predictions)
 };
 
 namespace dfuse_cuda {

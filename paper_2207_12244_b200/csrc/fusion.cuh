@@ -52,6 +52,17 @@ struct BandNb {
 struct FusionArgs {
   int W, H;
   const double* pred[6];
+  // float32 copies of prediction planes 1..5 (log_depth_var, grad_x,
+  // grad_x_var, grad_y, grad_y_var) when their values are float-exact, as
+  // DFPRED values always are (predictions.hpp:16-17, 201-203); pred[0] (the
+  // log-depth, shifted by focal_adjust in double) stays fp64. pred_f32 = 1:
+  // the sweeps read these (24 instead of 48 bytes of prediction data per
+  // pixel and sweep) and form the reciprocal variances on the fly, with the
+  // same div_nr as the per-call planes: bit-identical results (modes in
+  // fusion_impl.cuh, SweepPlanesT).
+  const float* predf[6];
+  int pred_f32_ok;  // predf holds every value exactly (set at keyframe creation)
+  int pred_f32;     // the sweeps' plane mode (SweepPlanesT), set per launch
   const double* sd;
   const double* sv;
   const uint8_t* svalid;

@@ -1,5 +1,7 @@
 // fusion_launch.cuh -- definition of launch_fusion_t (fusion_part_*.cu only)
 #pragma once
+#include <stdio.h>
+
 #include "fusion_impl.cuh"
 
 namespace dfuse_cuda {
@@ -11,16 +13,39 @@ void launch_fusion_t(dfuse_ctx* ctx, FusionArgs& a, int grid) {
   size_t smem = 0;
   if (PPT > 0) {
     smem = pcg_tile_smem(PPT, a.tw_max, a.th_max);
-    size_t& configured = ctx->fusion_smem_set[PPT * 4 + VAR];  // per context = per device
-    if (smem > configured) {
+    // The attribute belongs to the (device, function) pair, shared by every
+    // context on the device: always the same value (the largest tile's
+    // need), so no context can lower it under another's launch. The flag is
+    // per context, i.e. per device.
+    size_t& configured = ctx->fusion_smem_set[PPT * 4 + VAR];
+    if (!configured) {
+      cudaFuncAttributes fa{};
+      DF_CUDA(cudaFuncGetAttributes(&fa, (const void*)k_fusion<PPT, VAR>));
+      int optin = 0;
+      DF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                                     ctx->device));
+      configured = (size_t)optin - fa.sharedSizeBytes;
       DF_CUDA(cudaFuncSetAttribute((const void*)k_fusion<PPT, VAR>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      configured = smem;
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)configured));
     }
+    if (smem > configured) throw CudaFailure{cudaErrorInvalidValue, "k_fusion tile smem"};
   }
   void* args[] = {&a};
-  DF_CUDA(cudaLaunchCooperativeKernel((const void*)k_fusion<PPT, VAR>, dim3(grid), dim3(FT), args,
-                                      smem, ctx->stream));
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_fusion<PPT, VAR>, dim3(grid),
+                                                    dim3(FT), args, smem, ctx->stream);
+  if (e != cudaSuccess) {  // say why (occupancy of this instantiation at this smem)
+    cudaGetLastError();
+    int occ = -1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fusion<PPT, VAR>, FT, smem);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, (const void*)k_fusion<PPT, VAR>);
+    fprintf(stderr,
+            "dfuse: k_fusion<%d,%d> launch failed (%s): grid %d, dynamic smem %zu (attribute "
+            "%d), static smem %zu, regs %d, blocks/SM %d\n",
+            PPT, VAR, cudaGetErrorString(e), grid, smem, fa.maxDynamicSharedSizeBytes,
+            fa.sharedSizeBytes, fa.numRegs, occ);
+    throw CudaFailure{e, "cudaLaunchCooperativeKernel(k_fusion)"};
+  }
 }
 
 }  // namespace dfuse_cuda

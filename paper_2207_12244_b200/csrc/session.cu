@@ -247,8 +247,9 @@ void kf_alloc(dfuse_keyframe* kf, const dfuse_intrinsics* K) {
   kf->grid = fusion_grid(ctx);
   const size_t dP = al(sizeof(double) * P);
   const bool resident = fusion_resident_possible(P, kf->grid);
-  const size_t total = 2 * al(sizeof(float) * P) + al(P) + al(sizeof(int) * P) + 2 * dP +
-                       al(P) + 256 + 11 * dP + 12 * dP + al(fusion_slots_bytes(kf->grid)) +
+  const size_t fP = al(sizeof(float) * P);
+  const size_t total = 2 * fP + al(P) + al(sizeof(int) * P) + 2 * dP + al(P) + 256 + 11 * dP +
+                       5 * fP + 12 * dP + al(fusion_slots_bytes(kf->grid)) +
                        al(sizeof(FusionControl)) + al(2 * sizeof(FusionStateDev)) +
                        (resident ? al(fusion_halo_bytes(P)) : 0);
   DF_CUDA(cudaMalloc(&kf->block, total));
@@ -271,6 +272,8 @@ void kf_alloc(dfuse_keyframe* kf, const dfuse_intrinsics* K) {
   f.W = kf->W;
   f.H = kf->H;
   for (int c = 0; c < 6; ++c) f.pred[c] = (double*)take(dP);
+  for (int c = 1; c < 6; ++c) f.predf[c] = (float*)take(sizeof(float) * P);
+  f.pred_f32_ok = 0;
   f.sd = kf->semi_d;
   f.sv = kf->semi_v;
   f.svalid = kf->semi_valid;
@@ -307,6 +310,13 @@ void kf_alloc(dfuse_keyframe* kf, const dfuse_intrinsics* K) {
 void kf_finish(dfuse_keyframe* kf, const float* I0, double texture_threshold) {
   dfuse_ctx* ctx = kf->ctx;
   const long P = kf->P;
+  // prediction planes 1..5 as float32 when every value is float-exact (the
+  // reference keeps them at float precision: predictions.hpp:16-17)
+  int* inexact = kf->counters + 6;
+  DF_CUDA(cudaMemsetAsync(inexact, 0, sizeof(int), ctx->stream));
+  launch_pred_narrow(ctx, kf->fa.pred, const_cast<float* const*>(kf->fa.predf), P, inexact);
+  int h_inexact = 0;
+  DF_CUDA(cudaMemcpyAsync(&h_inexact, inexact, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   DF_CUDA(cudaMemcpyAsync(kf->I0, I0, sizeof(float) * P, cudaMemcpyHostToDevice, ctx->stream));
   launch_texture_mask(ctx, kf->I0, kf->W, kf->H, texture_threshold, kf->mask);
   launch_mask_list(ctx, kf->mask, P, kf->list, kf->counters + 1);
@@ -315,6 +325,7 @@ void kf_finish(dfuse_keyframe* kf, const float* I0, double texture_threshold) {
   clear_sync(kf);
   reset_state(kf);
   DF_CUDA(cudaStreamSynchronize(ctx->stream));
+  kf->fa.pred_f32_ok = (h_inexact == 0 && ctx->pred_fp32) ? 1 : 0;
 }
 
 void check_kf_args(const dfuse_intrinsics* K, const float* I0, double texture_threshold) {

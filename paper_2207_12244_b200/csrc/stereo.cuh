@@ -52,6 +52,11 @@ void launch_mask_list(dfuse_ctx* ctx, const uint8_t* mask, long P, int* list, in
 void launch_stereo(dfuse_ctx* ctx, const StereoArgs& a, bool list_mode,
                    bool counter_zeroed = false);
 void launch_count_valid(dfuse_ctx* ctx, const uint8_t* valid, long P, int* out);
+// float32 copies of prediction planes 1..5 over [0, n) (the caller shifts
+// the pointers); *inexact += the values that do not survive the round trip
+// through float (then the fp64 planes must be used)
+void launch_pred_narrow(dfuse_ctx* ctx, const double* const* planes64, float* const* planes32,
+                        long n, int* inexact);
 void launch_compact_obs(dfuse_ctx* ctx, const uint8_t* flag, const dfuse_obs* dense, long P,
                         int* block_scratch, dfuse_obs* out);
 void launch_update_list(dfuse_ctx* ctx, const dfuse_obs* obs, int n, int w, int h, int* head,

@@ -175,3 +175,35 @@ def test_host_async_pipeline_equals_sync_frames(orc):
     assert res.stereo_frames == len(seq.frames)
     kf.close()
     ctx.close()
+
+
+@pytest.mark.parametrize("name,bands", [("C2", 0), ("S", 0), ("S", 3)])
+def test_fp32_prediction_planes_are_bit_identical(orc, name, bands):
+    """Float-exact prediction planes kept as float32 on the device
+    (dfuse_ctx_set_fp32_predictions, default) give the same fused state, bit
+    for bit, as the fp64 planes: the values are identical and the reciprocal
+    variances are formed by the same division."""
+    import ctypes as C
+
+    spec = synth.small_spec(160, 120, frames=3) if name == "S" else synth.CONFIGS["C2"]
+    seq = synth.make_sequence(spec, 13, frames=3)
+    cfg = RobustConfig(gn_iterations=spec.gn_iterations)
+    out = {}
+    L = api.lib()
+    L.dfuse_ctx_set_fp32_predictions.argtypes = [C.c_void_p, C.c_int]
+    for on in (1, 0):
+        ctx = api.Context(0)
+        assert L.dfuse_ctx_set_fp32_predictions(ctx.handle, on) == 0
+        if bands:
+            kf = api.BandedKeyframe(ctx, spec.camera(), seq.I0, seq.pred, bands, 0.02)
+        else:
+            kf = api.Keyframe(ctx, spec.camera(), seq.I0, seq.pred, 0.02)
+        pcg = []
+        for (q, t, I1) in seq.frames:
+            g = orc.make_epipolar_geometry(synth.IDENTITY_Q, np.zeros(3), q, t, spec.camera())
+            pcg.append(kf.process_frame(g, I1, spec.search, cfg, "full").stats.pcg_total)
+        st, semi, _ = kf.download()
+        out[on] = (pcg, st.log_depth.tobytes(), st.scale, st.iteration, semi.depth.tobytes())
+        kf.close()
+        ctx.close()
+    assert out[1] == out[0]
