@@ -56,7 +56,6 @@ struct dfuse_ctx {
   int stereo_occ = 0;             // resident k_stereo CTAs per SM
   int fusion_occ = 0;             // resident k_fusion CTAs per SM
   size_t tex_base_align = 0, tex_pitch_align = 0;
-  size_t fusion_smem_set[64] = {};  // dynamic smem attribute set per k_fusion instantiation
   int pred_fp32 = 1;  // sessions keep float-exact prediction planes as fp32 (dfuse_ctx_set_fp32_predictions)
 };
 

@@ -277,9 +277,8 @@ void plan_tiles(FusionArgs& a, int grid) {
 void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
   plan_tiles(a, grid);
   if (ctx->force_streaming == 1) a.ppt = 0;
-  // prediction planes (SweepPlanesT): fp32 gradients, and fp32 variances
-  // with the reciprocals in the sweeps when streaming from HBM
-  a.pred_f32 = a.pred_f32_ok ? (a.ppt > 0 ? 2 : 1) : 0;
+  // prediction planes (SweepPlanesT): the fp32 copies when streaming from HBM
+  a.pred_f32 = a.pred_f32_ok && a.ppt == 0 ? 1 : 0;
   a.pcg_variant = ctx->force_streaming == 2 ? 2 : (ctx->force_streaming == 3 ? 1 : 0);
   {  // scale-round staging lives in the resident PCG's shared memory
     const long range = ((long)a.W * a.H + grid - 1) / grid;

@@ -2,11 +2,14 @@
 #pragma once
 #include <stdio.h>
 
+#include <mutex>
+
 #include "fusion_impl.cuh"
 
 namespace dfuse_cuda {
 
 constexpr size_t kMaxDynSmem = 227 * 1024;
+constexpr int kMaxDevices = 64;
 
 template <int PPT, int VAR>
 void launch_fusion_t(dfuse_ctx* ctx, FusionArgs& a, int grid) {
@@ -14,21 +17,19 @@ void launch_fusion_t(dfuse_ctx* ctx, FusionArgs& a, int grid) {
   if (PPT > 0) {
     smem = pcg_tile_smem(PPT, a.tw_max, a.th_max);
     // The attribute belongs to the (device, function) pair, shared by every
-    // context on the device: always the same value (the largest tile's
-    // need), so no context can lower it under another's launch. The flag is
-    // per context, i.e. per device.
-    size_t& configured = ctx->fusion_smem_set[PPT * 4 + VAR];
-    if (!configured) {
-      cudaFuncAttributes fa{};
-      DF_CUDA(cudaFuncGetAttributes(&fa, (const void*)k_fusion<PPT, VAR>));
-      int optin = 0;
-      DF_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin,
-                                     ctx->device));
-      configured = (size_t)optin - fa.sharedSizeBytes;
+    // context and thread on the device: one process-wide table per device,
+    // raised (never lowered) under a lock, to the largest tile launched so
+    // far.
+    static std::mutex mu;
+    static size_t set[kMaxDevices] = {};
+    if (ctx->device < 0 || ctx->device >= kMaxDevices)
+      throw CudaFailure{cudaErrorInvalidDevice, "k_fusion attribute table"};
+    std::lock_guard<std::mutex> lk(mu);
+    if (smem > set[ctx->device]) {
       DF_CUDA(cudaFuncSetAttribute((const void*)k_fusion<PPT, VAR>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)configured));
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      set[ctx->device] = smem;
     }
-    if (smem > configured) throw CudaFailure{cudaErrorInvalidValue, "k_fusion tile smem"};
   }
   void* args[] = {&a};
   const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_fusion<PPT, VAR>, dim3(grid),
