@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(FT, 2) k_fusion_banded(BandLaunch L) {  // as 
   c.nband = L.nband;
   c.rank_slots = L.rank_slots;
   c.sys = L.sys;
-  const Range rg = my_range(a);
+  const Range rg = my_range<true>(a);  // the band's CTAs walk it interleaved
   const Sel sel = terms_for(a.mode);
   FusionControl* ctl = a.ctl;
   const bool leader = c.me == 0 && threadIdx.x == 0;  // each band's own control block
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(FT, 1) k_gradient(FusionArgs a, double* g) {
   const double* ld = a.ld[0];
   PlainLd L{ld};
   double cost = 0.0, gs = 0.0;
-  for (int i = rg.beg + threadIdx.x; i < rg.end; i += FT) {
+  for (int i = rg.first(FT); i < rg.end; i += rg.stride(FT)) {
     const int y = i / W, x = i - y * W;
     const double li = ld[i];
     double gi = 0.0;
