@@ -343,9 +343,10 @@ void launch_fusion(dfuse_ctx* ctx, FusionArgs& a, int grid) {
     fprintf(stderr,
             "dfuse trace (ppt %d, ns, CTA 0): ring %.0f spmv %.0f ar/wait_rz %.0f pq_upd %.0f "
             "ar_pq %.0f sweep %.0f | scale %lld strial %lld assemble %lld pcg %lld dtrial %lld "
-            "(pcg its %d) sm_clock %.0f MHz | trial sweeps only: scale %lld depth %lld\n",
+            "(pcg its %d) sm_clock %.0f MHz | trial sweeps only: scale %lld depth %lld | "
+            "prefetched all-reduce waits that polled (poll warps, all CTAs, cumulative) %lld\n",
             a.ppt, ns[0], ns[1], ns[2], ns[3], ns[4], ns[5], tr[8], tr[9], tr[10], tr[11], tr[12],
-            its, 1e3 * ghz, tr[13], tr[14]);
+            its, 1e3 * ghz, tr[13], tr[14], tr[15]);
     if (a.dbg && ctx->trace >= 3) {  // each CTA's view of its all-reduces (SM cycles)
       std::vector<long long> h(dbg_n);
       DF_CUDA(cudaMemcpy(h.data(), a.dbg, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost));

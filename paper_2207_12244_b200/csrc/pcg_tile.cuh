@@ -465,6 +465,8 @@ __device__ int pcg_resident_pipe(GridCtx& c, const FusionArgs& a, double bnorm2,
   double r_gp = rcp_nr(gamma_prev), r_al = 1.0;
   int streak = 0, status = 0;
   *its = 0;
+  // prefetched all-reduce waits: one slot per polling lane
+  const bool pf = DFUSE_AR_PREFETCH && c.G <= 32u * kPollWarps;
   for (int it = 0;; ++it) {
     // s_z holds m_it (halo from array (it+1)&1, flag base+it+2); mr := H m_it
     const bool more = it < a.cg_max;
@@ -472,15 +474,24 @@ __device__ int pcg_resident_pipe(GridCtx& c, const FusionArgs& a, double bnorm2,
       // no barrier before the interior SpMV: the one in the last publish
       // (cta_partial) follows every thread's s_z writes of the update sweep
       t.template spmv<false>(mr, mr);
+      if (pf && DFUSE_AR_PREFETCH == 1) grid_allreduce_prefetch<3>(c);
       trc.mark(1);
       t.ring(a, hb0 + (long)((it + 1) & 1) * 2 * P, base + (unsigned)it + 2u);
+      // the all-reduce's slot words start towards shared memory now, while
+      // the boundary SpMV runs (grid_allreduce_wait_prefetched). Issued
+      // after the interior SpMV instead (DFUSE_AR_PREFETCH=1): 501 vs 504
+      // updates/s at C2 defaults (the earlier copy finds more flags unset)
+      if (pf && DFUSE_AR_PREFETCH == 2) grid_allreduce_prefetch<3>(c);
       __syncthreads();
       trc.mark(0);
       t.template spmv<true>(mr, mr);
       trc.mark(1);
     }
     double v[3];  // (r.u, w.u, r.r) of the vectors after `it` updates
-    grid_allreduce_wait(c, v);
+    if (pf && more)
+      grid_allreduce_wait_prefetched(c, v);
+    else
+      grid_allreduce_wait(c, v);
     trc.mark(2);
     double gamma, beta, pq;
     if (it == 0) {
