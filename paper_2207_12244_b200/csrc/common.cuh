@@ -65,7 +65,7 @@ namespace dfuse_cuda {
 enum Slot {
   S_IMG0, S_IMG1, S_MASK, S_SEMI_D, S_SEMI_V, S_SEMI_VALID, S_STATUS, S_BEST, S_NSTEPS, S_OBS,
   S_LIST, S_COUNTERS, S_PRED, S_LD, S_FUSION_WS, S_PARTIALS, S_BARRIER, S_CONTROL, S_PX,
-  S_PRIOR, S_HASPRIOR, S_TMP0, S_TMP1, S_TMP2, S_TMP3, S_TMP4, S_NUM
+  S_PRIOR, S_HASPRIOR, S_TMP0, S_TMP1, S_TMP2, S_TMP3, S_TMP4, S_QUEUE, S_QCOUNT, S_NUM
 };
 
 void* scratch(dfuse_ctx* ctx, int slot, size_t bytes);  // throws CudaFailure

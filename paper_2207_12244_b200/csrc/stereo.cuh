@@ -13,6 +13,9 @@ struct SearchResult {
   int n_steps;
 };
 
+// a pixel of the scan that reaches the step loop (stereo.cu)
+struct StereoItem;
+
 struct StereoArgs {
   dfuse_epigeom g;
   dfuse_search_cfg cfg;
@@ -39,6 +42,9 @@ struct StereoArgs {
   int32_t* n_steps;
   dfuse_obs* obs;
   uint8_t* obs_flag;
+  // scan mode: the searches queued by the preamble (set by launch_stereo)
+  StereoItem* queue;
+  int* queue_count;
 };
 
 void launch_photometric(dfuse_ctx* ctx, const dfuse_epigeom& g, const float* I0, const float* I1,
