@@ -685,7 +685,8 @@ def main():
         mf = measure(ctx, streams, cfg_f, args, device, ws, red_dev, flush, cstream, False)
         sf = summarize(mf, P, jobs, args)
         fixed = (cfg_f, mf, sf)
-    ar_us = allreduce_floor_us(ctx) if s["ppt"] > 0 else None
+    # the all-reduce floor, only where the latency roofline uses it
+    ar_us = allreduce_floor_us(ctx) if s["ppt"] > 0 and fixed is not None else None
 
     if rank != 0:
         if ws > 1:
