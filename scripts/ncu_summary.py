@@ -89,7 +89,7 @@ def main():
         except OSError:
             rec = {}
         for r, n in zip(data, names):
-            short = n.split("::")[-1].split("<")[0]
+            short = n.split("::")[-1].split("<")[0].replace("void ", "").strip()
             rd = num(r[col["dram__bytes_read.sum"]]) or 0.0
             wr = num(r[col["dram__bytes_write.sum"]]) or 0.0
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}

@@ -16,7 +16,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $O/${T}_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline \
     --no-e2e --no-fixed > $O/${T}_ncu_launch.log 2>&1
 # one full capture of each hot kernel (frame 2: a heavy stereo frame)
-ncu --set full --import-source on --clock-control none -k regex:"k_stereo|k_fusion" -s 4 -c 2 \
+ncu --set full --import-source on --clock-control none -k regex:"^(k_stereo|k_fusion)$" -s 4 -c 2 \
     -o $O/prof_${T} python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-fixed \
     > $O/${T}_ncu_full.log 2>&1
 # the streaming solver at 4K (fixed effort: one optimize of 500 GN x 5 PCG)
