@@ -176,6 +176,61 @@ struct PcgTile {
     }
   }
 
+  // The ring with its words prefetched: ring_prefetch (thread t takes ring
+  // cell t) starts cp.async copies of the cells' LL words into a shared
+  // staging area, issued part-way through the interior SpMV, when the
+  // neighbours have usually posted; ring_finish waits for the copies and
+  // keeps the words whose flags are `flag`, polling L2 only for the others.
+  __device__ __forceinline__ static unsigned long long* ring_stage() {
+    __shared__ unsigned long long st[2 * FT];
+    return st;
+  }
+  __device__ __forceinline__ void ring_cell(const FusionArgs& a, int t, int& g, int& so) const {
+    int gx, gy;
+    if (t < tg.tw) {
+      gx = tg.x0 + t, gy = tg.y0 - 1, so = t + 1;
+    } else if (t < 2 * tg.tw) {
+      gx = tg.x0 + t - tg.tw, gy = tg.y0 + tg.th, so = (tg.th + 1) * pw + t - tg.tw + 1;
+    } else if (t < 2 * tg.tw + tg.th) {
+      gx = tg.x0 - 1, gy = tg.y0 + t - 2 * tg.tw, so = (t - 2 * tg.tw + 1) * pw;
+    } else {
+      gx = tg.x0 + tg.tw, gy = tg.y0 + t - 2 * tg.tw - tg.th,
+      so = (t - 2 * tg.tw - tg.th + 1) * pw + tg.tw + 1;
+    }
+    g = gy * a.W + gx;
+    if (!(gx >= 0 && gx < a.W && gy >= 0 && gy < a.H)) so = -1;
+  }
+  __device__ __forceinline__ void ring_prefetch(const FusionArgs& a,
+                                                const unsigned long long* z_ll) const {
+    const int ring_n = T > 0 ? 2 * (tg.tw + tg.th) : 0;
+    if ((int)threadIdx.x < ring_n) {
+      int g, so;
+      ring_cell(a, threadIdx.x, g, so);
+      if (so >= 0) cp_async16(ring_stage() + 2 * threadIdx.x, z_ll + 2 * (long)g);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  __device__ __forceinline__ void ring_finish(const FusionArgs& a, const unsigned long long* z_ll,
+                                              unsigned flag) const {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    const int ring_n = T > 0 ? 2 * (tg.tw + tg.th) : 0;
+    if ((int)threadIdx.x < ring_n) {
+      int g, so;
+      ring_cell(a, threadIdx.x, g, so);
+      if (so >= 0) {
+        const unsigned long long w0 = ring_stage()[2 * threadIdx.x];
+        const unsigned long long w1 = ring_stage()[2 * threadIdx.x + 1];
+        const bool hit = (unsigned)(w0 >> 32) == flag && (unsigned)(w1 >> 32) == flag;
+        s_z()[so] = hit ? ll_value(w0, w1) : ll_wait(z_ll + 2 * (long)g, flag);
+      }
+    }
+    for (int t = threadIdx.x + FT; t < ring_n; t += FT) {
+      int g, so;
+      ring_cell(a, t, g, so);
+      if (so >= 0) s_z()[so] = ll_wait(z_ll + 2 * (long)g, flag);
+    }
+  }
+
   // post the tile's own boundary cells of the halo'd plane (s_z) as LL
   // words (version `flag`): one thread per perimeter cell (corners twice,
   // same value), after a barrier that follows the plane's writes
@@ -201,10 +256,10 @@ struct PcgTile {
   // w = H z, StencilMatrix::apply order (fusion.hpp:127-131), branch-free.
   // BOUNDARY selects the pass: false = interior pixels (own-tile z only, can
   // run before the halo ring arrives), true = tile-boundary pixels
-  template <bool BOUNDARY>
+  template <bool BOUNDARY, int J0 = 0, int J1 = PPT>
   __device__ __forceinline__ void spmv(const double (&zr)[PPT], double (&wv)[PPT]) const {
 #pragma unroll
-    for (int j = 0; j < PPT; ++j) {
+    for (int j = J0; j < J1; ++j) {
       if (valid(j) && boundary(j) == BOUNDARY) {
         const int k = threadIdx.x + FT * j, so = this->so(j);
         double v = s_diag()[k] * zr[j];
@@ -473,10 +528,22 @@ __device__ int pcg_resident_pipe(GridCtx& c, const FusionArgs& a, double bnorm2,
     if (more) {
       // no barrier before the interior SpMV: the one in the last publish
       // (cta_partial) follows every thread's s_z writes of the update sweep
-      t.template spmv<false>(mr, mr);
+      const unsigned long long* hr = hb0 + (long)((it + 1) & 1) * 2 * P;
+      if (DFUSE_RING_PF > 0 && DFUSE_RING_PF < PPT) {
+        // the ring's words start towards shared memory part-way through the
+        // interior SpMV (DFUSE_RING_PF of the PPT slots done)
+        t.template spmv<false, 0, (DFUSE_RING_PF < PPT ? DFUSE_RING_PF : 0)>(mr, mr);
+        t.ring_prefetch(a, hr);
+        t.template spmv<false, (DFUSE_RING_PF < PPT ? DFUSE_RING_PF : 0), PPT>(mr, mr);
+      } else {
+        t.template spmv<false>(mr, mr);
+      }
       if (pf && DFUSE_AR_PREFETCH == 1) grid_allreduce_prefetch<3>(c);
       trc.mark(1);
-      t.ring(a, hb0 + (long)((it + 1) & 1) * 2 * P, base + (unsigned)it + 2u);
+      if (DFUSE_RING_PF > 0 && DFUSE_RING_PF < PPT)
+        t.ring_finish(a, hr, base + (unsigned)it + 2u);
+      else
+        t.ring(a, hr, base + (unsigned)it + 2u);
       // the all-reduce's slot words start towards shared memory now, while
       // the boundary SpMV runs (grid_allreduce_wait_prefetched). Issued
       // after the interior SpMV instead (DFUSE_AR_PREFETCH=1): 501 vs 504
