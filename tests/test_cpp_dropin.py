@@ -109,3 +109,16 @@ def test_reference_scan_loop_through_dropin(tmp_path, orc):
     assert var.tobytes() == semi.variance.tobytes()
     assert valid.tobytes() == semi.valid.tobytes()
     assert cnt == semi.inlier_count
+
+
+def test_stereo_scan_template_matches_the_reference_shape():
+    """dfuse::gpu::stereo_scan instantiates with types shaped like the
+    reference's Keyframe / Frame / PipelineConfig (compile only)."""
+    src = os.path.join(ROOT, "tests", "cpp", "test_scan_template.cpp")
+    out = os.path.join(ROOT, "build", "test_scan_template")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    r = subprocess.run(["g++", "-std=c++20", "-O1", "-I" + os.path.join(ROOT, "include"),
+                        "-I" + os.path.join(ROOT, "include", "compat"), src, "-o", out,
+                        "-L" + LIBDIR, "-ldfuse_cuda", "-Wl,-rpath," + LIBDIR],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-4000:]

@@ -173,3 +173,26 @@ def test_c4_4k_streaming_and_bands(gpu_ctx, c4_case, bands):
     compare_frame(res, kf, ref[0])
     assert res.stats.pcg_total == ref[0][3] == 10
     kf.close()
+
+
+@pytest.mark.parametrize("name,frames", [("C1", 5), ("C5", 20)])
+def test_free_running_sequences(gpu_ctx, orc, name, frames):
+    """bench.py's other lines, free-running over their whole sequences: C1
+    (320x240, 50 GN iterations, 5 frames) and C5 (textureless regions,
+    Laplace priors, search range 0.1-20 m, 20 frames)."""
+    spec = synth.CONFIGS[name]
+    seq = synth.make_sequence(spec, 0, frames=frames)
+    cfg = RobustConfig(gn_iterations=spec.gn_iterations)
+    geoms = _geoms(orc, spec, seq)
+    ref = oracle_pipeline(orc, spec, seq, cfg, geoms)
+    kf = api.Keyframe(gpu_ctx, spec.camera(), seq.I0, seq.pred, 0.02)
+    # C1 runs 50 GN iterations: the late ones solve for a right-hand side
+    # (the cost gradient at convergence) whose terms cancel to ~1e-6 of their
+    # size, so the ulp-level differences of the assembly (SURVEY App. B, H7/H8)
+    # move each late solve's PCG count by up to 3 (every GPU data path gives the
+    # same counts; scripts/pcg_count_diag.py): 5 % per frame there, while the
+    # fused state stays within the 1e-4 bar
+    pcg_tol = 0.05 if spec.gn_iterations > 10 else 0.02
+    for k, (g, (_, _, I1)) in enumerate(zip(geoms, seq.frames)):
+        compare_frame(kf.process_frame(g, I1, spec.search, cfg, "full"), kf, ref[k], pcg_tol)
+    kf.close()
