@@ -414,7 +414,7 @@ void create_bkf(dfuse_banded_keyframe* kf, const dfuse_intrinsics* K, const floa
   kf->rank = rank;
   // CTAs per band: two per SM overall, like the streaming kernel (whose
   // reductions a one-band keyframe then reproduces bit for bit)
-  kf->cpr = 2 * fusion_grid(ctx) / per_process;
+  kf->cpr = band_ctas_per_sm() * fusion_grid(ctx) / per_process;
   if (kf->cpr > 32 * 5 * 2) kf->cpr = 32 * 5 * 2;
   const long P = kf->P;
   const size_t common = 2 * al(sizeof(float) * P) + al(P) + al(sizeof(int) * bands + 256) +

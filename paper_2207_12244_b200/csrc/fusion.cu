@@ -26,7 +26,10 @@ struct BandLaunch {
   int nband, cpr, band0, sys;
 };
 
-__global__ void __launch_bounds__(FT, 2) k_fusion_banded(BandLaunch L) {  // as k_fusion<0, 0>
+#ifndef DFUSE_BAND_MINB
+#define DFUSE_BAND_MINB 2  // CTAs per SM of the row-band solve (bands.cu sizes its grid by it)
+#endif
+__global__ void __launch_bounds__(FT, DFUSE_BAND_MINB) k_fusion_banded(BandLaunch L) {
   __shared__ FusionArgs s_args;  // fields survive the L1 invalidation of every fence
   const int band = L.band0 + (int)(blockIdx.x / L.cpr);
   if (threadIdx.x == 0) s_args = L.args[band];
@@ -89,6 +92,8 @@ void launch_fusion_banded(dfuse_ctx* ctx, const FusionArgs* args_dev,
                                       argv, 0, ctx->stream));
   DF_LAUNCHED(ctx);
 }
+
+int band_ctas_per_sm() { return DFUSE_BAND_MINB; }
 
 size_t band_rank_slots_bytes(int nband) {
   return sizeof(unsigned long long) * kSlotWords * 8 * (size_t)nband;

@@ -119,6 +119,7 @@ void launch_fusion_banded(dfuse_ctx* ctx, const FusionArgs* args_dev,
                           unsigned long long* const* rank_slots_dev, int nband, int cpr,
                           int band0, int nlocal, int sys);
 size_t band_rank_slots_bytes(int nband);
+int band_ctas_per_sm();  // resident CTAs per SM of k_fusion_banded
 void launch_stencil_apply(dfuse_ctx* ctx, int W, int H, const double* diag, const double* right,
                           const double* down, const double* x, double* y);
 
