@@ -389,6 +389,12 @@ class BandedKeyframe(Keyframe):
     def process_frame_async(self, *a, **k):
         raise NotImplementedError("the row-band keyframe has no asynchronous frame call")
 
+    def process_frame_host_async(self, *a, **k):
+        raise NotImplementedError("the row-band keyframe has no pipelined host-frame call")
+
+    def last_result(self):
+        raise NotImplementedError("the row-band keyframe has no asynchronous frame call")
+
     def process_frame(self, g: EpiGeom, I1, search: SearchConfig | None = None,
                       robust: RobustConfig | None = None, mode="full", device_ptr=None):
         search = search or SearchConfig()
