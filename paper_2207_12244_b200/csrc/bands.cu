@@ -309,7 +309,7 @@ void process_bkf(dfuse_banded_keyframe* kf, const dfuse_epigeom* g, const float*
   DF_CUDA(cudaMemcpyAsync(kf->d_args, args.data(), sizeof(FusionArgs) * kf->nband,
                           cudaMemcpyHostToDevice, ctx->stream));
   launch_fusion_banded(ctx, kf->d_args, kf->d_rank, kf->nband, kf->cpr, first, nlocal,
-                       kf->rank >= 0 ? 1 : 0);
+                       kf->rank >= 0 ? 1 : 0, &args[first]);
   DF_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
   for (Band& b : kf->bands)
     if (b.local)

@@ -83,9 +83,66 @@ __global__ void __launch_bounds__(FT, DFUSE_BAND_MINB) k_fusion_banded(BandLaunc
   }
 }
 
+// One band in this launch (one band per GPU, or a one-band keyframe): the
+// band's FusionArgs travel as a kernel parameter, like k_fusion's, so every
+// field is a constant-bank operand; k_fusion_banded's shared-memory copy
+// made each one a register load and spilled 2 KB per thread at the
+// 64-register cap.
+struct BandLaunch1 {
+  FusionArgs a;
+  unsigned long long* const* rank_slots;  // [nband] level-2 LL arrays
+  int nband, cpr, band, sys;
+};
+
+__global__ void __launch_bounds__(FT, DFUSE_BAND_MINB) k_fusion_band1(BandLaunch1 L) {
+  const FusionArgs& a = L.a;
+  BandCtx c;
+  c.slots = a.slots;
+  c.G = (unsigned)L.cpr;
+  c.base_tag = 0;
+  c.phase = a.persist_sync ? a.ctl->sync_phase : 0u;  // as k_fusion_banded
+  c.syncs = 0;
+  c.ll_next = 1;
+  c.me = blockIdx.x;
+  c.band = L.band;
+  c.nband = L.nband;
+  c.rank_slots = L.rank_slots;
+  c.sys = L.sys;
+  const Range rg = my_range<true>(a);
+  const Sel sel = terms_for(a.mode);
+  FusionControl* ctl = a.ctl;
+  const bool leader = c.me == 0 && threadIdx.x == 0;
+  if (c.me == 0) {
+    for (int k = threadIdx.x; k < DFUSE_STATS_MAX_GN; k += FT) {
+      ctl->stats.pcg_iters[k] = -1;
+      ctl->stats.scale_step[k] = -1.0;
+      ctl->stats.depth_step[k] = -1.0;
+    }
+    __syncthreads();
+  }
+  sweep_prologue(a, rg);
+  double v[1] = {c.me == 0 && threadIdx.x == 0 ? (double)*a.inlier_dev : 0.0};
+  grid_allreduce(c, v);  // fenced, and the keyframe's inlier count
+  int status = 0;
+  optimize_body<0, 0>(c, a, rg, sel, leader, status, (int)v[0]);
+  if (leader) {
+    ctl->status = status;
+    ctl->stats.grid_syncs = c.syncs;
+    if (a.persist_sync) ctl->sync_phase = c.phase;
+  }
+}
+
 void launch_fusion_banded(dfuse_ctx* ctx, const FusionArgs* args_dev,
                           unsigned long long* const* rank_slots_dev, int nband, int cpr,
-                          int band0, int nlocal, int sys) {
+                          int band0, int nlocal, int sys, const FusionArgs* args_host) {
+  if (nlocal == 1 && args_host) {
+    BandLaunch1 L{*args_host, rank_slots_dev, nband, cpr, band0, sys};
+    void* argv[] = {&L};
+    DF_CUDA(cudaLaunchCooperativeKernel((const void*)k_fusion_band1, dim3(cpr), dim3(FT), argv, 0,
+                                        ctx->stream));
+    DF_LAUNCHED(ctx);
+    return;
+  }
   BandLaunch L{args_dev, rank_slots_dev, nband, cpr, band0, sys};
   void* argv[] = {&L};
   DF_CUDA(cudaLaunchCooperativeKernel((const void*)k_fusion_banded, dim3(nlocal * cpr), dim3(FT),

@@ -115,9 +115,11 @@ void launch_gradient(dfuse_ctx* ctx, FusionArgs& a, int grid, double* g);
 // row-band optimize: args_dev[nband] (device), one cooperative launch of
 // nband * cpr CTAs (fusion.cu, k_fusion_banded)
 // (bands band0 .. band0 + nlocal - 1 of nband; sys: bands on several GPUs)
+// args_host: the host copy of the local bands' args (one local band runs
+// the parameter-space kernel k_fusion_band1)
 void launch_fusion_banded(dfuse_ctx* ctx, const FusionArgs* args_dev,
                           unsigned long long* const* rank_slots_dev, int nband, int cpr,
-                          int band0, int nlocal, int sys);
+                          int band0, int nlocal, int sys, const FusionArgs* args_host);
 size_t band_rank_slots_bytes(int nband);
 int band_ctas_per_sm();  // resident CTAs per SM of k_fusion_banded
 void launch_stencil_apply(dfuse_ctx* ctx, int W, int H, const double* diag, const double* right,
