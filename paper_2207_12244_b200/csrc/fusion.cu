@@ -252,6 +252,10 @@ static unsigned long long next_tag() {
 }
 
 constexpr size_t kMaxDynSmem = 227 * 1024;  // also in fusion_launch.cuh
+// static shared memory of the resident kernels (all-reduce and ring prefetch
+// staging, reduction scratch: 18 KB at 384 threads), kept out of the tile's
+// dynamic budget
+constexpr size_t kResidentStaticSmem = 20 * 1024;
 
 int fusion_grid(dfuse_ctx* ctx) {
   int& occ = ctx->fusion_occ;
@@ -330,7 +334,8 @@ void plan_tiles(FusionArgs& a, int grid) {
   const long T = (long)a.tw_max * a.th_max;
   constexpr long R = kResidentFT;
   a.ppt = T <= 4 * R ? 4 : (T <= 5 * R ? 5 : (T <= DFUSE_PPT_HI * R ? DFUSE_PPT_HI : 0));
-  if (a.ppt > 0 && pcg_tile_smem(a.ppt, a.tw_max, a.th_max) > kMaxDynSmem) a.ppt = 0;
+  if (a.ppt > 0 && pcg_tile_smem(a.ppt, a.tw_max, a.th_max) > kMaxDynSmem - kResidentStaticSmem)
+    a.ppt = 0;
   // LL flags are 32-bit: the whole launch must fit
   if ((double)a.gn * ((double)a.cg_max + 2.0) > 2.0e9) a.ppt = 0;
   if (!a.halo) a.ppt = 0;
