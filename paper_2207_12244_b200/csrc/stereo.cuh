@@ -22,6 +22,7 @@ struct StereoArgs {
   const float* I0;
   const float* I1;
   cudaTextureObject_t tex1;  // set by launch_stereo (frame_texture)
+  double wm1, hm1;           // width - 1.0, height - 1.0 (set by launch_stereo)
   int n_items;
   int* work_counter;
   // scan mode: masked-pixel list + semi map (in/out)
