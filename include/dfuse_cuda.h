@@ -173,7 +173,10 @@ int64_t dfuse_ctx_texture_launches(const dfuse_ctx* ctx);
 int dfuse_ctx_set_fp32_predictions(dfuse_ctx* ctx, int on);
 /* diagnostics: device time (ms) of one cooperative launch running n grid-wide
  * all-reduces of the fusion solver on `grid` CTAs (variant 10 = production LL
- * all-to-all, 2 = atomic arrival counter) */
+ * all-to-all, 2 = atomic arrival counter; 11-16 = two-level over CTA pairs,
+ * cluster launch: 11/13 pair stage spinning on a DSMEM LL word, 12/14 the
+ * same with only the even CTAs polling, 15 = variant 10 under a cluster
+ * launch, 16 = pair stage by st.async on an mbarrier) */
 int dfuse_debug_sync_bench(dfuse_ctx* ctx, int n, int variant, int grid, float* ms);
 /* the context's cudaStream_t (for timing with events on the launch stream) */
 void* dfuse_ctx_stream(const dfuse_ctx* ctx);

@@ -244,6 +244,235 @@ __global__ void __launch_bounds__(FT, 1) k_sync_bench(ReduceSlot* slots, unsigne
   if (blockIdx.x == 0 && threadIdx.x == 0) *out = acc;
 }
 
+// Two-level all-reduce over CTA pairs (clusters of 2; microbenchmark
+// variants 11 and 12): the odd CTA of a pair sends its partial to the even
+// one through distributed shared memory (one LL pair per value); the even
+// CTA posts the pair's sum as one LL slot. Variant 11: every CTA polls the
+// G/2 pair slots. Variant 12: only the even CTAs poll, and each forwards the
+// total to its partner through distributed shared memory.
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+template <bool WEAK>
+__device__ __forceinline__ void dsmem_put_v2(void* local_addr, unsigned rank, unsigned long long a,
+                                             unsigned long long b) {
+  const unsigned la = (unsigned)__cvta_generic_to_shared(local_addr);
+  unsigned ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(rank));
+  if (WEAK)
+    asm volatile("st.shared::cluster.v2.u64 [%0], {%1, %2};" ::"r"(ra), "l"(a), "l"(b)
+                 : "memory");
+  else
+    asm volatile("st.relaxed.cluster.shared::cluster.v2.u64 [%0], {%1, %2};" ::"r"(ra), "l"(a),
+                 "l"(b)
+                 : "memory");
+}
+template <bool WEAK>
+__device__ __forceinline__ double smem_ll_wait(const unsigned long long* p, unsigned flag) {
+  const unsigned la = (unsigned)__cvta_generic_to_shared(p);
+  unsigned long long w0, w1;
+  do {
+    if (WEAK)
+      asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];"
+                   : "=l"(w0), "=l"(w1)
+                   : "r"(la)
+                   : "memory");
+    else
+      asm volatile("ld.relaxed.cluster.shared::cta.v2.u64 {%0, %1}, [%2];"
+                   : "=l"(w0), "=l"(w1)
+                   : "r"(la)
+                   : "memory");
+  } while ((unsigned)(w0 >> 32) != flag || (unsigned)(w1 >> 32) != flag);
+  return ll_value(w0, w1);
+}
+
+template <int NV, int VARIANT>
+__device__ void pair_allreduce(GridCtx& c, double (&v)[NV]) {
+  __shared__ double red[FW * 4];
+  __shared__ double pol[kPollWarps * 4];
+  __shared__ __align__(16) unsigned long long box[2][4][2];  // [0] partial in, [1] total in
+  constexpr bool WEAK = VARIANT >= 13;  // weak DSMEM store, volatile local poll
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned rank = cluster_rank(), pair = blockIdx.x >> 1, P2 = c.G >> 1;
+  const unsigned flag = c.phase + 1;
+  double t[NV];
+  cta_partial(v, t, red);
+  if (wid == 0 && lane < NV) {
+    double tk = t[0];
+#pragma unroll
+    for (int k = 1; k < NV; ++k)
+      if (lane == k) tk = t[k];
+    if (rank == 1) {
+      dsmem_put_v2<WEAK>(&box[0][lane][0], 0, ll_word(tk, 0, flag), ll_word(tk, 1, flag));
+    } else {
+      const double other = smem_ll_wait<WEAK>(&box[0][lane][0], flag);
+      const double ps = tk + other;  // rank order
+      st_relaxed_v2(ll_slot(c, c.phase, lane, pair), ll_word(ps, 0, flag),
+                    ll_word(ps, 1, flag));
+    }
+  }
+  const bool poller = VARIANT == 11 || VARIANT == 13 || rank == 0;
+  if (poller && wid < kPollWarps) {
+    double acc[NV];
+    for (;;) {
+      bool ok = true;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+#pragma unroll
+      for (int m = 0; m < kMaxPollSlots; ++m) {
+        const unsigned b = lane + 32 * (wid + kPollWarps * m);
+        if (b < P2) {
+#pragma unroll
+          for (int k = 0; k < NV; ++k) {
+            unsigned long long w0, w1;
+            ld_relaxed_v2(ll_slot(c, c.phase, k, b), w0, w1);
+            ok &= (unsigned)(w0 >> 32) == flag && (unsigned)(w1 >> 32) == flag;
+            acc[k] += ll_value(w0, w1);
+          }
+        }
+      }
+      if (__all_sync(0xffffffffu, ok)) break;
+    }
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] = warp_sum(acc[k]);
+    if (lane == 0)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) pol[wid * 4 + k] = acc[k];
+  }
+  if (VARIANT == 12 || VARIANT == 14) {
+    if (rank == 0) {
+      __syncthreads();
+      if (wid == 0 && lane < NV) {
+        double s = pol[lane];
+        for (int w = 1; w < kPollWarps; ++w) s += pol[w * 4 + lane];
+        dsmem_put_v2<WEAK>(&box[1][lane][0], 1, ll_word(s, 0, flag), ll_word(s, 1, flag));
+      }
+    } else if (wid == 0 && lane < NV) {
+      const double s = smem_ll_wait<WEAK>(&box[1][lane][0], flag);
+      pol[lane] = s;
+      for (int w = 1; w < kPollWarps; ++w) pol[w * 4 + lane] = 0.0;
+    }
+  }
+  __syncthreads();
+  poll_total(pol, v);
+  c.phase += 1;
+  c.syncs += 1;
+}
+
+// variant 16: the pair stage as st.async into the even CTA's buffer,
+// completing bytes on its mbarrier (hardware wait instead of a spin)
+template <int NV>
+__device__ void pair_allreduce_mbar(GridCtx& c, double (&v)[NV], unsigned long long* mbar,
+                                    double* buf) {
+  __shared__ double red[FW * 4];
+  __shared__ double pol[kPollWarps * 4];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned rank = cluster_rank(), pair = blockIdx.x >> 1, P2 = c.G >> 1;
+  const unsigned flag = c.phase + 1;
+  double t[NV];
+  cta_partial(v, t, red);
+  if (wid == 0) {
+    double tk = t[0];
+#pragma unroll
+    for (int k = 1; k < NV; ++k)
+      if (lane == k) tk = t[k];
+    const unsigned mb = (unsigned)__cvta_generic_to_shared(mbar);
+    if (rank == 1) {
+      if (lane < NV) {
+        const unsigned lb = (unsigned)__cvta_generic_to_shared(buf + lane);
+        unsigned rb, rm;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rb) : "r"(lb));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rm) : "r"(mb));
+        asm volatile(
+            "st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(rb),
+            "l"(__double_as_longlong(tk)), "r"(rm)
+            : "memory");
+      }
+    } else {
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
+                     "r"(8 * NV)
+                     : "memory");
+      unsigned done = 0;
+      const unsigned par = c.phase & 1;
+      do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; "
+            "selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(mb), "r"(par)
+            : "memory");
+      } while (!done);
+      if (lane < NV) {
+        const double ps = tk + buf[lane];  // rank order
+        st_relaxed_v2(ll_slot(c, c.phase, lane, pair), ll_word(ps, 0, flag),
+                      ll_word(ps, 1, flag));
+      }
+    }
+  }
+  if (wid < kPollWarps) {
+    double acc[NV];
+    for (;;) {
+      bool ok = true;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+      const unsigned b = lane + 32 * wid;
+      if (b < P2) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          unsigned long long w0, w1;
+          ld_relaxed_v2(ll_slot(c, c.phase, k, b), w0, w1);
+          ok &= (unsigned)(w0 >> 32) == flag && (unsigned)(w1 >> 32) == flag;
+          acc[k] += ll_value(w0, w1);
+        }
+      }
+      if (__all_sync(0xffffffffu, ok)) break;
+    }
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] = warp_sum(acc[k]);
+    if (lane == 0)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) pol[wid * 4 + k] = acc[k];
+  }
+  __syncthreads();
+  poll_total(pol, v);
+  c.phase += 1;
+  c.syncs += 1;
+}
+
+template <int VARIANT>
+__global__ void __launch_bounds__(FT, 1) k_sync_bench_pair(ReduceSlot* slots, int n, double* out) {
+  GridCtx c{slots, gridDim.x, 0ull, 0u, 0, 1u};
+  __shared__ __align__(8) unsigned long long mbar;
+  __shared__ double mbuf[4];
+  if (VARIANT == 16) {
+    if (threadIdx.x == 0) {
+      const unsigned mb = (unsigned)__cvta_generic_to_shared(&mbar);
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+  }
+  double acc = 0.0;
+  for (int i = 0; i < n; ++i) {
+    double v[2] = {1.0, (double)threadIdx.x};
+    if (VARIANT == 16)
+      pair_allreduce_mbar<2>(c, v, &mbar, mbuf);
+    else if (VARIANT == 15)  // the flat LL all-reduce under a cluster launch
+      grid_allreduce<2, false, 10>(c, v);
+    else
+      pair_allreduce<2, VARIANT>(c, v);
+    acc += v[0];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *out = acc;
+  // no CTA leaves while its partner may still address its shared memory
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // host side
 static unsigned long long next_tag() {
@@ -472,9 +701,38 @@ float sync_bench(dfuse_ctx* ctx, int n, int variant, int grid) {
   DF_CUDA(cudaMemsetAsync(slots, 0, bytes, ctx->stream));
   unsigned long long tag = next_tag();
   void* args[] = {&slots, &tag, &n, &out};
-  const void* fn = variant == 2 ? (const void*)k_sync_bench<2> : (const void*)k_sync_bench<10>;
   DF_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
-  DF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(FT), args, 0, ctx->stream));
+  if (variant >= 11 && variant <= 16) {  // clusters of 2 (grid rounded down to even)
+    grid &= ~1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(FT);
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    if (variant == 11)
+      DF_CUDA(cudaLaunchKernelEx(&cfg, k_sync_bench_pair<11>, slots, n, out));
+    else if (variant == 12)
+      DF_CUDA(cudaLaunchKernelEx(&cfg, k_sync_bench_pair<12>, slots, n, out));
+    else if (variant == 13)
+      DF_CUDA(cudaLaunchKernelEx(&cfg, k_sync_bench_pair<13>, slots, n, out));
+    else if (variant == 14)
+      DF_CUDA(cudaLaunchKernelEx(&cfg, k_sync_bench_pair<14>, slots, n, out));
+    else if (variant == 15)
+      DF_CUDA(cudaLaunchKernelEx(&cfg, k_sync_bench_pair<15>, slots, n, out));
+    else
+      DF_CUDA(cudaLaunchKernelEx(&cfg, k_sync_bench_pair<16>, slots, n, out));
+  } else {
+    const void* fn = variant == 2 ? (const void*)k_sync_bench<2> : (const void*)k_sync_bench<10>;
+    DF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(FT), args, 0, ctx->stream));
+  }
   DF_LAUNCHED(ctx);
   DF_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
   DF_CUDA(cudaEventSynchronize(ctx->ev[1]));

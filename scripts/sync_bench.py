@@ -22,8 +22,9 @@ L = api.lib()
 L.dfuse_debug_sync_bench.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int,
                                      C.POINTER(C.c_float)]
 ms = C.c_float()
-for variant in (10, 2):
-    for grid in (32, 74, 148):
+only = [int(a) for a in sys.argv[1:]]
+for variant in only or (10, 11, 12, 2):
+    for grid in (74, 148) if variant in (11, 12, 13, 14, 15, 16) else (32, 74, 148):
         t = {}
         L.dfuse_debug_sync_bench(ctx.handle, 50000, variant, grid, C.byref(ms))  # clock warm-up
         for n in (0, 20000):
@@ -35,6 +36,8 @@ for variant in (10, 2):
             t[n] = best
         print(json.dumps({"what": "allreduce", "variant": variant, "grid": grid,
                           "us_per_op": round((t[20000] - t[0]) * 1e3 / 20000, 3)}), flush=True)
+if only:
+    sys.exit(0)
 
 # PCG per-iteration cost at 640x480 (fixed iteration counts)
 st, semi, pred = make_random_problem(5, 640, 480)
