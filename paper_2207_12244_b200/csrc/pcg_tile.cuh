@@ -50,6 +50,11 @@
 // every parity case, 2 % faster at C2).
 #pragma once
 
+#ifndef DFUSE_TASM_UNROLL
+#define DFUSE_TASM_UNROLL 2  // pixel slots per step of the tile-order assembly (1/2/3/6 measured)
+#endif
+constexpr int kTasmUnroll = DFUSE_TASM_UNROLL;
+
 // shared-memory carve-up and per-thread pixel map of one tile
 template <int PPT>
 struct PcgTile {
@@ -150,6 +155,74 @@ struct PcgTile {
         zr[j] = z;
         s_z()[so(j)] = z;
         if (bd) ll_store(z_ll + 2 * (long)g, z, flag);
+      }
+    }
+  }
+
+  // Tile-order assembly (the pipelined solve's default): every own pixel's
+  // diag and four couplings go straight into the tile's planes, b is parked
+  // in s_p for load_assembled, and nothing is written to global memory --
+  // no coupling raster, no re-read, no fence before the solve. Per-pixel
+  // arithmetic is assemble_pixel's, as in the raster-order sweep; the left
+  // and up couplings are formed by the pixel itself with the expressions
+  // its neighbours use for their right and down ones.
+  template <class PL>
+  __device__ __forceinline__ void assemble(const FusionArgs& a, const Sel sel,
+                                           const double* __restrict__ ld, const double ln_s,
+                                           const PL pl, double (&v)[4]) {
+    map(a);
+    double bn = 0.0, rz = 0.0, bad = 0.0, cost = 0.0;
+#pragma unroll kTasmUnroll
+    for (int j = 0; j < PPT; ++j) {
+      const int k = threadIdx.x + FT * j;
+      if (k < T) {
+        const int ly = k / tg.tw, lx = k - ly * tg.tw;
+        const int x = tg.x0 + lx, y = tg.y0 + ly;
+        const AsmPixel e = assemble_pixel(y * a.W + x, x, y, a.W, a.H, sel, a.dnet, a.dsemi,
+                                          a.dgrad, ld, ln_s, pl);
+        s_diag()[k] = e.diag;
+        s_right()[k] = e.right;
+        s_left()[k] = e.left;
+        s_down()[k] = e.down;
+        s_up()[k] = e.up;
+        s_p()[k] = e.b;
+        const double z = div_nr(e.b, e.diag);  // PCG init z = r/diag, fusion.hpp:329
+        bn += e.b * e.b;
+        if (!(e.diag > 0.0)) bad += 1.0;
+        rz += e.b * z;
+        cost += e.cost;
+      }
+    }
+    v[0] = bn;
+    v[1] = rz;
+    v[2] = bad;
+    v[3] = cost;
+  }
+
+  // load() for a tile assembled in place: r from s_p, then as load()
+  __device__ __forceinline__ void load_assembled(const FusionArgs& a, double (&rr_)[PPT],
+                                                 double (&zr)[PPT], unsigned long long* z_ll,
+                                                 unsigned flag) {
+    map(a);
+    for (int t = threadIdx.x; t < (tg.th + 2) * pw; t += FT) s_z()[t] = 0.0;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      const int k = threadIdx.x + FT * j;
+      rr_[j] = zr[j] = 0.0;
+      if (valid(j)) {
+        const double d = s_diag()[k];
+        const double rd = rcp_nr(d);
+        s_rdiag()[k] = rd;
+        const double r = s_p()[k];
+        s_p()[k] = 0.0;
+        s_x()[k] = 0.0;
+        rr_[j] = r;
+        const double q0 = r * rd;  // z = r/diag, fusion.hpp:329
+        const double z = __fma_rn(__fma_rn(-q0, d, r), rd, q0);
+        zr[j] = z;
+        s_z()[so(j)] = z;
+        if (boundary(j)) ll_store(z_ll + 2 * (long)gi(j), z, flag);
       }
     }
   }
@@ -475,7 +548,7 @@ struct PcgHandover {
 // memory, the PcgTrace accumulators still open)
 template <int PPT>
 __device__ int pcg_resident_pipe(GridCtx& c, const FusionArgs& a, double bnorm2, double rz,
-                                 int* its, PcgHandover* hand) {
+                                 int* its, PcgHandover* hand, bool assembled) {
   PcgTile<PPT> t;
   const long P = (long)a.W * a.H;
   // LL array v: a.halo + v 2P (v = 0, 1; arithmetic, not an indexed local array)
@@ -484,7 +557,10 @@ __device__ int pcg_resident_pipe(GridCtx& c, const FusionArgs& a, double bnorm2,
   const unsigned base = c.ll_next;
   c.ll_next += (unsigned)a.cg_max + 3u;
   double rr_[PPT], mr[PPT], wr[PPT], zr[PPT], sr[PPT];
-  t.load(a, rr_, mr, hb0, base + 1);  // mr = u0 = r0/diag, in s_z with halo
+  if (assembled)  // mr = u0 = r0/diag, in s_z with halo
+    t.load_assembled(a, rr_, mr, hb0, base + 1);
+  else
+    t.load(a, rr_, mr, hb0, base + 1);
   PcgTrace trc(a);
   // w0 = H u0
   __syncthreads();

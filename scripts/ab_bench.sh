@@ -13,6 +13,7 @@ for r in 1 2; do
 import json,sys
 d=json.loads(sys.stdin.read()); f=d.get('fixed_effort') or {}
 print('$lib', 'value', d['value'], 'fixed', f.get('value'), 'stereo_ms', d['stage_ms']['stereo'],
-      'opt_ms', d['stage_ms']['optimise'], 'fixed_stereo_ms', (f.get('stage_ms') or {}).get('stereo'))"
+      'opt_ms', d['stage_ms']['optimise'], 'fixed_opt_ms', (f.get('stage_ms') or {}).get('optimise'),
+      'pcg', d.get('pcg_iters_per_update'))"
   done
 done
