@@ -199,6 +199,25 @@ struct PcgTile {
     v[3] = cost;
   }
 
+  // the global rasters (diag, right, down, r) of the standalone solve into
+  // the tile's planes, as assemble() leaves them (r parked in s_p)
+  __device__ __forceinline__ void stage_global(const FusionArgs& a) {
+    map(a);
+    const int W = a.W, H = a.H;
+    for (int j = 0; j < PPT; ++j) {
+      const int k = threadIdx.x + FT * j;
+      if (valid(j)) {
+        const int g = gi(j), gy = g / W, gx = g - gy * W;
+        s_diag()[k] = __ldcg(a.diag + g);
+        s_right()[k] = gx + 1 < W ? __ldcg(a.right + g) : 0.0;
+        s_left()[k] = gx > 0 ? __ldcg(a.right + g - 1) : 0.0;
+        s_down()[k] = gy + 1 < H ? __ldcg(a.down + g) : 0.0;
+        s_up()[k] = gy > 0 ? __ldcg(a.down + g - W) : 0.0;
+        s_p()[k] = __ldcg(a.r + g);
+      }
+    }
+  }
+
   // load() for a tile assembled in place: r from s_p, then as load()
   __device__ __forceinline__ void load_assembled(const FusionArgs& a, double (&rr_)[PPT],
                                                  double (&zr)[PPT], unsigned long long* z_ll,
@@ -557,10 +576,8 @@ __device__ int pcg_resident_pipe(GridCtx& c, const FusionArgs& a, double bnorm2,
   const unsigned base = c.ll_next;
   c.ll_next += (unsigned)a.cg_max + 3u;
   double rr_[PPT], mr[PPT], wr[PPT], zr[PPT], sr[PPT];
-  if (assembled)  // mr = u0 = r0/diag, in s_z with halo
-    t.load_assembled(a, rr_, mr, hb0, base + 1);
-  else
-    t.load(a, rr_, mr, hb0, base + 1);
+  if (!assembled) t.stage_global(a);
+  t.load_assembled(a, rr_, mr, hb0, base + 1);  // mr = u0 = r0/diag, in s_z with halo
   PcgTrace trc(a);
   // w0 = H u0
   __syncthreads();
