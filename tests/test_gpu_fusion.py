@@ -146,6 +146,20 @@ def test_optimize_random_problems(gpu, orc, mode):
         assert all(abs(x - y) <= 1 for x, y in zip(sa.pcg_iters, sb.pcg_iters))
 
 
+@pytest.mark.parametrize("mode", MODES)
+def test_optimize_zero_step_accepted(gpu, orc, mode):
+    """cg_max_iters = 0: every depth step is zero, the trial state is the
+    current one and the reference accepts it (cost equal to c0, fusion.hpp:
+    432-441); the same steps, costs evaluated and state on the device."""
+    st, semi, pred = make_random_problem(12, 96, 64, outlier_fraction=0.1)
+    cfg = RobustConfig(gn_iterations=4, cg_max_iters=0)
+    a, sa = gpu.optimize(st, semi, pred, cfg, mode, with_stats=True)
+    b, sb = orc.optimize(st, semi, pred, cfg, mode, with_stats=True)
+    _check_opt(a, b)
+    assert sa.depth_step == sb.depth_step
+    assert sa.pcg_iters == sb.pcg_iters == [0] * 4
+
+
 def test_optimize_kats(gpu):
     # test_fusion.cpp:85-99: anchored 1x2 chain
     st, semi, pred = blank_problem(2, 1)
