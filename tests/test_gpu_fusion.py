@@ -160,6 +160,22 @@ def test_optimize_zero_step_accepted(gpu, orc, mode):
     assert sa.pcg_iters == sb.pcg_iters == [0] * 4
 
 
+@pytest.mark.parametrize("gn,its", [(0, 200), (3, 1), (3, 2)])
+def test_optimize_short_budgets(gpu, orc, gn, its):
+    """No Gauss-Newton iteration (the state passes through unchanged), and
+    solves cut off after one or two PCG iterations (the pipelined loop's
+    first iterations end in its stop rules)."""
+    st, semi, pred = make_random_problem(13, 80, 56, outlier_fraction=0.1)
+    cfg = RobustConfig(gn_iterations=gn, cg_tol=0.0, cg_max_iters=its)
+    a, sa = gpu.optimize(st, semi, pred, cfg, with_stats=True)
+    b, sb = orc.optimize(st, semi, pred, cfg, with_stats=True)
+    _check_opt(a, b)
+    assert a.iteration == b.iteration == st.iteration + gn
+    assert sa.pcg_iters == sb.pcg_iters == [its] * gn
+    if gn == 0:
+        assert a.log_depth.tobytes() == st.log_depth.tobytes() and a.scale == st.scale
+
+
 def test_optimize_kats(gpu):
     # test_fusion.cpp:85-99: anchored 1x2 chain
     st, semi, pred = blank_problem(2, 1)
