@@ -308,6 +308,8 @@ def run_reference(args, spec, seq, steps, warmup, budget_s=120.0, keep_state_aft
     ref = oracle.reference()
     L = ref.lib
     L.ref_process_frame.restype = C.c_int
+    # all the host threads this process may use (torchrun sets OMP_NUM_THREADS=1)
+    L.ref_omp_set_threads(len(os.sched_getaffinity(0)))
     threads = L.ref_omp_max_threads()
     cfg = solver_cfg(spec, args.regime)
     mask = ref.texture_mask(seq.I0, 0.02)

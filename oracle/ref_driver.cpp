@@ -171,6 +171,17 @@ int ref_omp_max_threads(void) {
 #endif
 }
 
+// the OpenMP team size of the reference's parallel loops (torchrun exports
+// OMP_NUM_THREADS=1 to every rank; the reference arm runs on rank 0 alone
+// and takes the host's cores)
+void ref_omp_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 int ref_make_epipolar_geometry(const double q0[4], const double t0[3], const double q1[4],
                                const double t1[3], const dfuse_intrinsics* K, dfuse_epigeom* out) {
   const EpipolarGeometry g = make_epipolar_geometry(make_pose(q0, t0), make_pose(q1, t1), make_K(*K));
